@@ -1,0 +1,145 @@
+/*
+ * cavi.h -- C ABI of the B200-native CAVI engine (libcavi.so).
+ *
+ * Drop-in boundary for the reference's variational path, `tissuemix.vb`
+ * (reference pkg/src/tissuemix/vb.py:26-34 `__all__`).  The reference has no
+ * FFI of its own (it is pure Python); these are the entry points a ctypes
+ * binding of that module binds (paper_2401_10068_b200/_lib.py; INTEGRATION.md
+ * shows the stub).  Plain pointers and sizes only; all host buffers are
+ * borrowed for the duration of the call; every call is blocking and returns
+ * a status code (CV_OK on success), with the message in cv_last_error().
+ *
+ *   cv_dataset_create    <- tissuemix.model.Dataset construction (model.py:89-123)
+ *                           uploaded into HBM (one-time, per dataset)
+ *   cv_dataset_generate  <- model.random_profiles + model.synth_generate
+ *                           (model.py:224-270), Philox4x32-10 stream-exact
+ *   cv_init              <- vb.vb_init (vb.py:82-111)
+ *   cv_step              <- vb.vb_step (vb.py:129-198)  (+ vb_elbo of the result)
+ *   cv_elbo              <- vb.vb_elbo (vb.py:216-304)
+ *   cv_fit               <- vb.vb_fit  (vb.py:312-354)
+ *   cv_materialize       <- the per-gene VbState fields mu_beta / lam_beta /
+ *                           e_beta / e_bbt (vb.py:49-54), produced on demand
+ *   cv_batched_fit       <- many independent vb_fit calls (config 4)
+ *
+ * Status codes map to the reference's exceptions (linalg.py:46-69):
+ *   CV_ERR_NUMERIC   -> linalg.NumericError   (non-PD / singular after retry)
+ *   CV_ERR_NONFINITE -> FloatingPointError    (non-finite input)
+ *   CV_ERR_ARG       -> ValueError            (bad arguments)
+ *   CV_ERR_CUDA      -> RuntimeError          (CUDA / NCCL failure)
+ */
+#ifndef CAVI_H
+#define CAVI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CV_MAX_DIM 15 /* N <= 16 networks (d = N - 1) */
+#define CV_MAX_D2 (CV_MAX_DIM * CV_MAX_DIM)
+
+enum {
+  CV_OK = 0,
+  CV_ERR_NUMERIC = 1,
+  CV_ERR_NONFINITE = 2,
+  CV_ERR_ARG = 3,
+  CV_ERR_CUDA = 4,
+  CV_ERR_IMPROPER = 5 /* NumericError("Q(Lambda) is improper; dataset too small") */
+};
+
+/* storage layouts of the measurement stream in HBM */
+enum {
+  CV_STORE_F64 = 0, /* x = r - mu and D as fp64 (exact) */
+  CV_STORE_F32 = 1  /* x and D stored as fp32, fp64 math (the optional fp32 path) */
+};
+
+/* Prior constants (reference model.py:126-151).  Host pointers, borrowed. */
+typedef struct cv_hyper {
+  double a0, b0, q0;
+  int32_t n0;
+  int32_t d;
+  const double* K0;      /* (d,) */
+  const double* Lambda0; /* (d,d) row-major, SPD */
+} cv_hyper;
+
+/* A variational state (reference VbState, vb.py:39-66) minus the per-gene
+ * arrays, which are a pure function of the dataset and the `gen_*` fields
+ * ("generator": the expectations the sweep that produced the state used),
+ * plus the sums the next sweep and the bound need.  Fixed-size, so it can be
+ * checkpointed by value.  Matrices are row-major d x d inside the arrays. */
+typedef struct cv_state {
+  int32_t d;
+  int32_t n_iter;      /* sweeps taken to reach this state (0 = vb_init) */
+  int32_t status;      /* CV_OK or the error the producing call hit */
+  int32_t elbo_status; /* CV_OK, or the error vb_elbo of this state raises */
+  int64_t V;
+  double a_rho, b_rho, e_rho;
+  double k0k[CV_MAX_DIM];
+  double lam0l_inv[CV_MAX_D2];
+  double e_lam[CV_MAX_D2];
+  double e_lamk[CV_MAX_DIM];
+  double ln_det_lam0l_inv;
+  double elbo;  /* vb_elbo(state) */
+  double resid; /* sum_i (r-mu)^2 - 2(r-mu) D.E[b] + D.E[bb^T].D under this state */
+  double gen_c[CV_MAX_DIM];
+  double gen_A[CV_MAX_D2];    /* per-gene precision base: lam_beta_i = A + e_rho D D^T */
+  double gen_Ainv[CV_MAX_D2];
+  double gen_lnA;
+  double gen_e_rho;
+} cv_state;
+
+typedef struct cv_dataset cv_dataset;
+
+/* ---- library ---------------------------------------------------------- */
+int32_t cv_abi_version(void);
+const char* cv_last_error(void);
+int32_t cv_device_count(int32_t* n);
+
+/* ---- datasets (device-resident measurement streams) -------------------- */
+/* Upload genes [0, V) of (r, mu, D) (D row-major (V, d)) to `device`.
+ * `gene_lo`/`V_total` place this shard in a dataset of V_total genes
+ * (gene_lo = 0, V_total = V for a whole dataset). */
+int32_t cv_dataset_create(const double* r, const double* mu, const double* D, int64_t V, int32_t d,
+                          int64_t gene_lo, int64_t V_total, int32_t storage, int32_t device,
+                          cv_dataset** out);
+/* Genes [gene_lo, gene_lo+V) of the dataset random_profiles(RngStream(seed), V_total, N) +
+ * synth_generate(truth=(K, Lam, rho)) would produce, generated on the device. */
+int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V_total, int32_t n_networks,
+                            const double* K, const double* Lam, double rho, int32_t storage,
+                            int32_t device, cv_dataset** out);
+/* Copy back x = r - mu, r, mu and D (row-major) of the shard; any pointer may be
+ * NULL (r and mu exist for datasets made by create/generate, which keep them). */
+int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, double* D);
+int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo, int64_t* V_total,
+                        int32_t* storage, int64_t* device_bytes);
+void cv_dataset_destroy(cv_dataset* ds);
+
+/* ---- the CAVI path --------------------------------------------------- */
+int32_t cv_init(cv_dataset* ds, const cv_hyper* hp, cv_state* out);
+int32_t cv_step(cv_dataset* ds, const cv_hyper* hp, const cv_state* in, cv_state* out);
+int32_t cv_elbo(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* elbo);
+/* Trace arrays have room for max_iter entries; *n_iter receives the count. */
+int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+               double param_tol, cv_state* out, double* tr_elbo, double* tr_dk, double* tr_drho,
+               double* tr_dlam, int32_t* n_iter);
+/* Per-gene moments of genes [lo, hi) of state `st`; any output may be NULL.
+ * mu_beta (n,d), lam_beta (n,d,d), e_bbt (n,d,d), n = hi - lo. */
+int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int64_t lo, int64_t hi,
+                       double* mu_beta, double* lam_beta, double* e_bbt);
+
+/* ---- pinned host memory (for end-to-end uploads at DMA speed) --------- */
+int32_t cv_host_alloc(int64_t bytes, void** out);
+void cv_host_free(void* p);
+
+/* ---- measurement hooks (bench.py) ------------------------------------ */
+/* Run `warmup` then `sweeps` CAVI sweeps (ELBO on, no stop rule) from `st`
+ * on the dataset's stream; *ms_total = CUDA-event time of the timed sweeps,
+ * *ms_kernel = summed CUDA-event time of the fused-pass kernels alone. */
+int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int32_t warmup,
+                        int32_t sweeps, double* ms_total, double* ms_kernel, int32_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAVI_H */

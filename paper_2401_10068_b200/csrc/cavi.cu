@@ -1,0 +1,682 @@
+// cavi.cu -- host side of libcavi.so: dataset handles in HBM, the CAVI loop
+// as CUDA graphs of fused-pass kernels (no host sync per sweep), and the C ABI
+// declared in include/cavi.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gen.cuh"
+#include "control.cuh"
+
+using namespace cavi;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess) return fail(CV_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,        \
+                                       cudaGetErrorString(e_));                                       \
+  } while (0)
+
+}  // namespace
+
+// one per dimension, from pass_inst.cu compiled with -DCAVI_D=1..15
+#define DECL(D) cavi::PassFn cavi_pass_d##D(int storage);
+DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
+DECL(9) DECL(10) DECL(11) DECL(12) DECL(13) DECL(14) DECL(15)
+#undef DECL
+
+namespace {
+
+PassFn pass_for(int d, int storage) {
+  switch (d) {
+#define CASE(D) \
+  case D:       \
+    return cavi_pass_d##D(storage);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+    default:
+      return nullptr;
+  }
+}
+
+}  // namespace
+
+struct cv_dataset {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int d = 0, storage = 0;
+  int64_t V = 0, Vp = 0, gene_lo = 0, V_total = 0;
+  void* x = nullptr;
+  void* D = nullptr;
+  double* r_raw = nullptr;
+  double* mu_raw = nullptr;
+  int64_t n_chunks = 0, n_groups = 0, group_lo = 0, n_groups_total = 0, groups_per_octant = 1;
+  int oct_lo = 0, oct_hi = kOctants;
+  double* partials = nullptr;
+  double* gpartials = nullptr;
+  unsigned int* counters = nullptr;  // [n_groups] + gdone
+  int* flags = nullptr;              // [0] bad input bits, [1] scratch status
+  Ctl* ctl = nullptr;
+  Hyp* hyp = nullptr;
+  double* trace = nullptr;
+  int trace_cap = 0;
+  int grid = 0;
+  PassFn pass = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph = nullptr;
+  int graph_unroll = 0;
+  Ctl* h_ctl = nullptr;  // pinned mirror
+  int bad_input = 0;
+  size_t device_bytes = 0;
+};
+
+namespace {
+
+size_t elem(int storage) { return storage == CV_STORE_F32 ? sizeof(float) : sizeof(double); }
+
+int plan_and_alloc(cv_dataset* ds) {
+  const int ns = n_stats(ds->d);
+  ds->n_chunks = (ds->V + kChunk - 1) / kChunk;
+  ds->Vp = ds->n_chunks * kChunk;
+  ds->n_groups = (ds->n_chunks + kGroupChunks - 1) / kGroupChunks;
+  const int64_t tot_chunks = std::max<int64_t>(1, (ds->V_total + kChunk - 1) / kChunk);
+  ds->n_groups_total = (tot_chunks + kGroupChunks - 1) / kGroupChunks;
+  ds->groups_per_octant = (ds->n_groups_total + kOctants - 1) / kOctants;
+  const int64_t group_genes = (int64_t)kGroupChunks * kChunk;
+  if (ds->gene_lo % group_genes != 0) return fail(CV_ERR_ARG, "shard gene_lo %lld not group-aligned", (long long)ds->gene_lo);
+  ds->group_lo = ds->gene_lo / group_genes;
+  // octants this shard covers (must be whole octants unless the shard is the whole dataset)
+  const int64_t oct_genes = ds->groups_per_octant * group_genes;
+  if (ds->V == ds->V_total) {
+    ds->oct_lo = 0;
+    ds->oct_hi = kOctants;
+  } else {
+    if (ds->gene_lo % oct_genes != 0) return fail(CV_ERR_ARG, "shard not octant-aligned");
+    ds->oct_lo = (int)(ds->gene_lo / oct_genes);
+    int64_t hi = ds->gene_lo + ds->V;
+    int oh = (int)((hi + oct_genes - 1) / oct_genes);
+    if (hi == ds->V_total) {
+      // the last shard owns every remaining (possibly empty) octant
+      int span = 1;
+      while (span < kOctants - ds->oct_lo && ds->oct_lo % (2 * span) == 0 && ds->oct_lo + 2 * span <= kOctants) span *= 2;
+      oh = std::max(oh, ds->oct_lo + span);
+    }
+    ds->oct_hi = std::min(oh, kOctants);
+  }
+  const size_t es = elem(ds->storage);
+  CK(cudaSetDevice(ds->device));
+  CK(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
+  const size_t nx = (size_t)std::max<int64_t>(ds->Vp, 2);
+  CK(cudaMalloc(&ds->x, nx * es));
+  CK(cudaMalloc(&ds->D, nx * es * ds->d));
+  CK(cudaMalloc(&ds->partials, sizeof(double) * ns * std::max<int64_t>(ds->n_chunks, 1)));
+  CK(cudaMalloc(&ds->gpartials, sizeof(double) * ns * std::max<int64_t>(ds->n_groups, 1)));
+  CK(cudaMalloc(&ds->counters, sizeof(unsigned int) * (ds->n_groups + 1)));
+  CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + 1), ds->stream));
+  CK(cudaMalloc(&ds->flags, sizeof(int) * 4));
+  CK(cudaMemsetAsync(ds->flags, 0, sizeof(int) * 4, ds->stream));
+  CK(cudaMalloc(&ds->ctl, sizeof(Ctl)));
+  CK(cudaMalloc(&ds->hyp, sizeof(Hyp)));
+  CK(cudaMallocHost(&ds->h_ctl, sizeof(Ctl)));
+  for (auto& e : ds->ev) CK(cudaEventCreate(&e));
+  ds->device_bytes = nx * es * (1 + ds->d);
+  ds->pass = pass_for(ds->d, ds->storage);
+  if (!ds->pass) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", ds->d, kMaxD);
+  int dev_sms = 0, per_sm = 0;
+  CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ds->device));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ds->pass, kThreads, 0));
+  ds->grid = (int)std::max<int64_t>(1, std::min<int64_t>(ds->n_chunks, (int64_t)dev_sms * std::max(per_sm, 1)));
+  return CV_OK;
+}
+
+PassArgs pass_args(cv_dataset* ds, double* rank_out) {
+  PassArgs a;
+  a.x = ds->x;
+  a.D = ds->D;
+  a.Vp = ds->Vp;
+  a.n_chunks = ds->n_chunks;
+  a.n_groups = ds->n_groups;
+  a.group_lo = ds->group_lo;
+  a.n_groups_total = ds->n_groups_total;
+  a.groups_per_octant = ds->groups_per_octant;
+  a.oct_lo = ds->oct_lo;
+  a.oct_hi = ds->oct_hi;
+  a.partials = ds->partials;
+  a.gpartials = ds->gpartials;
+  a.gcount = ds->counters;
+  a.gdone = ds->counters + ds->n_groups;
+  a.ctl = ds->ctl;
+  a.hyp = ds->hyp;
+  a.rank_out = rank_out;
+  return a;
+}
+
+int launch_pass(cv_dataset* ds) {
+  if (ds->n_chunks == 0) return fail(CV_ERR_ARG, "empty shard");
+  ds->pass<<<ds->grid, kThreads, 0, ds->stream>>>(pass_args(ds, nullptr));
+  CK(cudaGetLastError());
+  return CV_OK;
+}
+
+int check_hyper(cv_dataset* ds, const cv_hyper* hp) {
+  if (!hp) return fail(CV_ERR_ARG, "null hyperparameters");
+  if (hp->d != ds->d) return fail(CV_ERR_ARG, "hyperparams dim %d != dataset dim %d", hp->d, ds->d);
+  if (!(hp->a0 > 0 && hp->b0 > 0 && hp->q0 > 0 && hp->n0 >= 1)) return fail(CV_ERR_ARG, "hyperparameters must be positive");
+  return CV_OK;
+}
+
+int upload_hyper(cv_dataset* ds, const cv_hyper* hp) {
+  int rc = check_hyper(ds, hp);
+  if (rc) return rc;
+  Hyp h;
+  std::memset(&h, 0, sizeof h);
+  h.d = hp->d;
+  h.n0 = hp->n0;
+  h.a0 = hp->a0;
+  h.b0 = hp->b0;
+  h.q0 = hp->q0;
+  h.V = (double)ds->V_total;
+  for (int i = 0; i < h.d; ++i) h.K0[i] = hp->K0[i];
+  for (int i = 0; i < h.d * h.d; ++i) h.L0[i] = hp->Lambda0[i];
+  CK(cudaSetDevice(ds->device));
+  CK(cudaMemcpyAsync(ds->hyp, &h, sizeof h, cudaMemcpyHostToDevice, ds->stream));
+  setup_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp);
+  CK(cudaGetLastError());
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, &ds->hyp->setup_status, sizeof st, cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  if (st != CV_OK) return fail(CV_ERR_NUMERIC, "Lambda0 is not positive definite");
+  if (ds->bad_input & 1) return fail(CV_ERR_NONFINITE, "non-finite values in A");
+  return CV_OK;
+}
+
+void reset_ctl(Ctl& c) {
+  std::memset(&c, 0, sizeof c);
+  c.max_iter = 0x7fffffff;
+  c.compute_elbo = 1;
+}
+
+int ctl_put(cv_dataset* ds, const Ctl& c) {
+  *ds->h_ctl = c;
+  CK(cudaMemcpyAsync(ds->ctl, ds->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, ds->stream));
+  return CV_OK;
+}
+
+int ctl_get(cv_dataset* ds) {
+  CK(cudaMemcpyAsync(ds->h_ctl, ds->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  return CV_OK;
+}
+
+// vb_init on the device: the init pass measures the prior moments (resid_0 and the bound).
+int run_init(cv_dataset* ds, int compute_elbo) {
+  Ctl c;
+  reset_ctl(c);
+  c.compute_elbo = compute_elbo;
+  int rc = ctl_put(ds, c);
+  if (rc) return rc;
+  init_gen_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
+  CK(cudaGetLastError());
+  return launch_pass(ds);
+}
+
+int status_code(int s) {
+  switch (s) {
+    case CV_OK:
+      return CV_OK;
+    case CV_ERR_NUMERIC:
+      return fail(CV_ERR_NUMERIC, "Q(Lambda) rate inversion failed after jitter retry (non-PD or non-finite)");
+    default:
+      return fail(s, "sweep failed with status %d", s);
+  }
+}
+
+int state_status(const cv_state& s) { return status_code(s.status); }
+
+int ensure_trace(cv_dataset* ds, int cap) {
+  if (ds->trace_cap >= cap) return CV_OK;
+  if (ds->trace) CK(cudaFree(ds->trace));
+  ds->trace = nullptr;
+  CK(cudaMalloc(&ds->trace, sizeof(double) * 4 * (size_t)cap));
+  ds->trace_cap = cap;
+  return CV_OK;
+}
+
+int ensure_graph(cv_dataset* ds, int unroll) {
+  if (ds->graph && ds->graph_unroll == unroll) return CV_OK;
+  if (ds->graph) CK(cudaGraphExecDestroy(ds->graph));
+  ds->graph = nullptr;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(ds->stream, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < unroll; ++i) ds->pass<<<ds->grid, kThreads, 0, ds->stream>>>(pass_args(ds, nullptr));
+  cudaError_t e = cudaStreamEndCapture(ds->stream, &g);
+  if (e != cudaSuccess) return fail(CV_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  CK(cudaGraphInstantiate(&ds->graph, g, 0));
+  CK(cudaGraphDestroy(g));
+  ds->graph_unroll = unroll;
+  return CV_OK;
+}
+
+template <typename T>
+int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, const double* D) {
+  // stage the host arrays in HBM, then transform into the SoA stream
+  double *dr = nullptr, *dmu = nullptr, *dD = nullptr;
+  const size_t V = (size_t)ds->V;
+  CK(cudaMalloc(&dr, sizeof(double) * std::max<size_t>(V, 1)));
+  CK(cudaMalloc(&dmu, sizeof(double) * std::max<size_t>(V, 1)));
+  CK(cudaMalloc(&dD, sizeof(double) * std::max<size_t>(V * ds->d, 1)));
+  CK(cudaMemcpyAsync(dr, r, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
+  CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
+  CK(cudaMemcpyAsync(dD, D, sizeof(double) * V * ds->d, cudaMemcpyHostToDevice, ds->stream));
+  const int tb = 256;
+  const int64_t blocks = (ds->Vp + tb - 1) / tb;
+  upload_kernel<T><<<(unsigned)blocks, tb, 0, ds->stream>>>(dr, dmu, dD, ds->V, ds->Vp, ds->d, (T*)ds->x, (T*)ds->D,
+                                                          ds->flags);
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ds->flags, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  ds->bad_input = bad;
+  ds->r_raw = dr;
+  ds->mu_raw = dmu;
+  CK(cudaFree(dD));
+  return CV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cv_abi_version(void) { return 1; }
+
+const char* cv_last_error(void) { return g_err.c_str(); }
+
+int32_t cv_device_count(int32_t* n) {
+  int k = 0;
+  cudaError_t e = cudaGetDeviceCount(&k);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return fail(CV_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *n = k;
+  return CV_OK;
+}
+
+void cv_dataset_destroy(cv_dataset* ds) {
+  if (!ds) return;
+  cudaSetDevice(ds->device);
+  if (ds->stream) cudaStreamSynchronize(ds->stream);
+  if (ds->graph) cudaGraphExecDestroy(ds->graph);
+  void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters,
+                  ds->flags, ds->ctl, ds->hyp, ds->trace};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (ds->h_ctl) cudaFreeHost(ds->h_ctl);
+  for (auto e : ds->ev)
+    if (e) cudaEventDestroy(e);
+  if (ds->stream) cudaStreamDestroy(ds->stream);
+  delete ds;
+}
+
+static int new_dataset(int64_t V, int32_t d, int64_t gene_lo, int64_t V_total, int32_t storage, int32_t device,
+                       cv_dataset** out) {
+  if (V < 1) return fail(CV_ERR_ARG, "empty dataset");
+  if (d < 1 || d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
+  if (storage != CV_STORE_F64 && storage != CV_STORE_F32) return fail(CV_ERR_ARG, "bad storage %d", storage);
+  if (gene_lo < 0 || V_total < gene_lo + V) return fail(CV_ERR_ARG, "shard [%lld, %lld) outside %lld genes",
+                                                      (long long)gene_lo, (long long)(gene_lo + V), (long long)V_total);
+  cv_dataset* ds = new cv_dataset();
+  ds->device = device;
+  ds->d = d;
+  ds->storage = storage;
+  ds->V = V;
+  ds->gene_lo = gene_lo;
+  ds->V_total = V_total;
+  int rc = plan_and_alloc(ds);
+  if (rc) {
+    std::string keep = g_err;
+    cv_dataset_destroy(ds);
+    g_err = keep;
+    return rc;
+  }
+  *out = ds;
+  return CV_OK;
+}
+
+int32_t cv_dataset_create(const double* r, const double* mu, const double* D, int64_t V, int32_t d, int64_t gene_lo,
+                          int64_t V_total, int32_t storage, int32_t device, cv_dataset** out) {
+  if (!r || !mu || !D || !out) return fail(CV_ERR_ARG, "null pointer");
+  cv_dataset* ds = nullptr;
+  int rc = new_dataset(V, d, gene_lo, V_total, storage, device, &ds);
+  if (rc) return rc;
+  rc = storage == CV_STORE_F32 ? create_storage_kernels<float>(ds, r, mu, D)
+                               : create_storage_kernels<double>(ds, r, mu, D);
+  if (rc) {
+    std::string keep = g_err;
+    cv_dataset_destroy(ds);
+    g_err = keep;
+    return rc;
+  }
+  *out = ds;
+  return CV_OK;
+}
+
+int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V_total, int32_t n_networks,
+                            const double* K, const double* Lam, double rho, int32_t storage, int32_t device,
+                            cv_dataset** out) {
+  if (!K || !Lam || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (n_networks < 2 || n_networks > kMaxD + 1) return fail(CV_ERR_ARG, "N must be in [2, %d]", kMaxD + 1);
+  if (!(rho > 0)) return fail(CV_ERR_ARG, "rho must be positive");
+  const int d = n_networks - 1;
+  cv_dataset* ds = nullptr;
+  int rc = new_dataset(V, d, gene_lo, V_total, storage, device, &ds);
+  if (rc) return rc;
+  auto bail = [&](int code) {
+    std::string keep = g_err;
+    cv_dataset_destroy(ds);
+    g_err = keep;
+    return code;
+  };
+  GenArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.seed = seed;
+  a.gene_lo = gene_lo;
+  a.V = V;
+  a.V_total = V_total;
+  a.Vp = ds->Vp;
+  a.N = n_networks;
+  a.d = d;
+  a.storage = storage;
+  for (int i = 0; i < d; ++i) a.K[i] = K[i];
+  a.sqrt_rho = std::sqrt(rho);
+  a.x = ds->x;
+  a.D = ds->D;
+  double* dLam = nullptr;
+  double* dL = nullptr;
+  if (cudaMalloc(&dLam, sizeof(double) * 2 * kMaxD2) != cudaSuccess) return bail(fail(CV_ERR_CUDA, "cudaMalloc"));
+  dL = dLam + kMaxD2;
+  if (cudaMalloc(&ds->r_raw, sizeof(double) * V) != cudaSuccess || cudaMalloc(&ds->mu_raw, sizeof(double) * V) != cudaSuccess) {
+    cudaFree(dLam);
+    return bail(fail(CV_ERR_CUDA, "cudaMalloc raw"));
+  }
+  a.r_raw = ds->r_raw;
+  a.mu_raw = ds->mu_raw;
+  int st = 0;
+  cudaMemcpyAsync(dLam, Lam, sizeof(double) * d * d, cudaMemcpyHostToDevice, ds->stream);
+  gen_prep_kernel<<<1, 1, 0, ds->stream>>>(dLam, dL, d, ds->flags + 1);
+  cudaMemcpyAsync(&st, ds->flags + 1, sizeof(int), cudaMemcpyDeviceToHost, ds->stream);
+  cudaError_t e = cudaStreamSynchronize(ds->stream);
+  if (e != cudaSuccess) {
+    cudaFree(dLam);
+    return bail(fail(CV_ERR_CUDA, "generator setup: %s", cudaGetErrorString(e)));
+  }
+  if (st != CV_OK) {
+    cudaFree(dLam);
+    return bail(fail(CV_ERR_NUMERIC, "truth Lambda not positive definite"));
+  }
+  const int tb = 256;
+  const unsigned blocks = (unsigned)((ds->Vp + tb - 1) / tb);
+  if (storage == CV_STORE_F32)
+    gen_kernel<float><<<blocks, tb, 0, ds->stream>>>(a, dL);
+  else
+    gen_kernel<double><<<blocks, tb, 0, ds->stream>>>(a, dL);
+  e = cudaStreamSynchronize(ds->stream);
+  cudaFree(dLam);
+  if (e != cudaSuccess) return bail(fail(CV_ERR_CUDA, "generator: %s", cudaGetErrorString(e)));
+  *out = ds;
+  return CV_OK;
+}
+
+int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, double* D) {
+  if (!ds) return fail(CV_ERR_ARG, "null dataset");
+  if ((r && !ds->r_raw) || (mu && !ds->mu_raw)) return fail(CV_ERR_ARG, "raw r/mu not kept for this dataset");
+  CK(cudaSetDevice(ds->device));
+  double *dx = nullptr, *dD = nullptr;
+  if (x) CK(cudaMalloc(&dx, sizeof(double) * ds->V));
+  if (D) CK(cudaMalloc(&dD, sizeof(double) * ds->V * ds->d));
+  const int tb = 256;
+  const unsigned blocks = (unsigned)((ds->V + tb - 1) / tb);
+  if (x || D) {
+    if (ds->storage == CV_STORE_F32)
+      download_kernel<float><<<blocks, tb, 0, ds->stream>>>((const float*)ds->x, (const float*)ds->D, ds->V, ds->Vp,
+                                                            ds->d, dx, dD);
+    else
+      download_kernel<double><<<blocks, tb, 0, ds->stream>>>((const double*)ds->x, (const double*)ds->D, ds->V,
+                                                             ds->Vp, ds->d, dx, dD);
+    CK(cudaGetLastError());
+  }
+  if (x) CK(cudaMemcpyAsync(x, dx, sizeof(double) * ds->V, cudaMemcpyDeviceToHost, ds->stream));
+  if (D) CK(cudaMemcpyAsync(D, dD, sizeof(double) * ds->V * ds->d, cudaMemcpyDeviceToHost, ds->stream));
+  if (r) CK(cudaMemcpyAsync(r, ds->r_raw, sizeof(double) * ds->V, cudaMemcpyDeviceToHost, ds->stream));
+  if (mu) CK(cudaMemcpyAsync(mu, ds->mu_raw, sizeof(double) * ds->V, cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  if (dx) CK(cudaFree(dx));
+  if (dD) CK(cudaFree(dD));
+  return CV_OK;
+}
+
+int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo, int64_t* V_total, int32_t* storage,
+                        int64_t* device_bytes) {
+  if (!ds) return fail(CV_ERR_ARG, "null dataset");
+  if (V) *V = ds->V;
+  if (d) *d = ds->d;
+  if (gene_lo) *gene_lo = ds->gene_lo;
+  if (V_total) *V_total = ds->V_total;
+  if (storage) *storage = ds->storage;
+  if (device_bytes) *device_bytes = (int64_t)ds->device_bytes;
+  return CV_OK;
+}
+
+int32_t cv_init(cv_dataset* ds, const cv_hyper* hp, cv_state* out) {
+  if (!ds || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (ds->V != ds->V_total) return fail(CV_ERR_ARG, "cv_init on a shard: use the sharded driver");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  rc = run_init(ds, 1);
+  if (rc) return rc;
+  rc = ctl_get(ds);
+  if (rc) return rc;
+  *out = ds->h_ctl->cur;
+  out->d = ds->d;
+  out->V = ds->V_total;
+  return state_status(*out);
+}
+
+int32_t cv_step(cv_dataset* ds, const cv_hyper* hp, const cv_state* in, cv_state* out) {
+  if (!ds || !in || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (in->d != ds->d || in->V != ds->V_total) return fail(CV_ERR_ARG, "state does not belong to this dataset");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  Ctl c;
+  reset_ctl(c);
+  c.cur = *in;
+  c.mode = MODE_SWEEP;
+  if ((rc = ctl_put(ds, c))) return rc;
+  derive_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
+  CK(cudaGetLastError());
+  if ((rc = launch_pass(ds))) return rc;
+  if ((rc = ctl_get(ds))) return rc;
+  *out = ds->h_ctl->cur;
+  return state_status(*out);
+}
+
+int32_t cv_elbo(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* elbo) {
+  if (!ds || !st || !elbo) return fail(CV_ERR_ARG, "null pointer");
+  if (st->d != ds->d || st->V != ds->V_total) return fail(CV_ERR_ARG, "state does not belong to this dataset");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  Ctl c;
+  reset_ctl(c);
+  c.cur = *st;
+  c.mode = MODE_ELBO;
+  if ((rc = ctl_put(ds, c))) return rc;
+  state_gen_kernel<<<1, 1, 0, ds->stream>>>(ds->ctl, ds->d);
+  CK(cudaGetLastError());
+  if ((rc = launch_pass(ds))) return rc;
+  if ((rc = ctl_get(ds))) return rc;
+  const cv_state& r = ds->h_ctl->cur;
+  if (r.elbo_status == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "Q(Lambda) is improper; dataset too small");
+  if (r.elbo_status != CV_OK) return fail(r.elbo_status, "bound evaluation failed (status %d)", r.elbo_status);
+  *elbo = r.elbo;
+  return CV_OK;
+}
+
+int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+               double param_tol, cv_state* out, double* tr_elbo, double* tr_dk, double* tr_drho, double* tr_dlam,
+               int32_t* n_iter) {
+  if (!ds || !out || !n_iter) return fail(CV_ERR_ARG, "null pointer");
+  if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
+  if (ds->V != ds->V_total) return fail(CV_ERR_ARG, "cv_fit on a shard: use the sharded driver");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  if ((rc = ensure_trace(ds, max_iter))) return rc;
+  Ctl c;
+  reset_ctl(c);
+  c.compute_elbo = compute_elbo ? 1 : 0;
+  c.max_iter = max_iter;
+  c.rel_tol = rel_tol;
+  c.param_tol = param_tol;
+  c.tr_cap = max_iter;
+  c.tr_elbo = ds->trace;
+  c.tr_dk = ds->trace + ds->trace_cap;
+  c.tr_drho = ds->trace + 2 * (size_t)ds->trace_cap;
+  c.tr_dlam = ds->trace + 3 * (size_t)ds->trace_cap;
+  if ((rc = ctl_put(ds, c))) return rc;
+  init_gen_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
+  CK(cudaGetLastError());
+  if ((rc = launch_pass(ds))) return rc;
+  // sweeps: unrolled graphs; every pass kernel exits at once after the stop rule fired
+  const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
+  if ((rc = ensure_graph(ds, unroll))) return rc;
+  int launched = 0;
+  for (;;) {
+    CK(cudaGraphLaunch(ds->graph, ds->stream));
+    launched += unroll;
+    CK(cudaMemcpyAsync(&ds->h_ctl->done, &ds->ctl->done, sizeof(int) * 4, cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaStreamSynchronize(ds->stream));
+    if (ds->h_ctl->done || launched >= max_iter) break;
+  }
+  if ((rc = ctl_get(ds))) return rc;
+  const Ctl& h = *ds->h_ctl;
+  *out = h.cur;
+  *n_iter = h.iter;
+  const size_t n = (size_t)h.iter;
+  if (tr_elbo) CK(cudaMemcpy(tr_elbo, c.tr_elbo, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (tr_dk) CK(cudaMemcpy(tr_dk, c.tr_dk, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (tr_drho) CK(cudaMemcpy(tr_drho, c.tr_drho, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (tr_dlam) CK(cudaMemcpy(tr_dlam, c.tr_dlam, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (h.status == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "Q(Lambda) is improper; dataset too small");
+  if (h.status != CV_OK) return status_code(h.status);
+  return CV_OK;
+}
+
+int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int64_t lo, int64_t hi,
+                       double* mu_beta, double* lam_beta, double* e_bbt) {
+  if (!ds || !st) return fail(CV_ERR_ARG, "null pointer");
+  if (lo < 0 || hi > ds->V || lo > hi) return fail(CV_ERR_ARG, "bad gene range");
+  (void)hp;
+  const int64_t n = hi - lo;
+  if (n == 0) return CV_OK;
+  const int d = ds->d;
+  Ctl c;
+  reset_ctl(c);
+  c.cur = *st;
+  int rc = ctl_put(ds, c);
+  if (rc) return rc;
+  double *dm = nullptr, *dl = nullptr, *de = nullptr;
+  if (mu_beta) CK(cudaMalloc(&dm, sizeof(double) * n * d));
+  if (lam_beta) CK(cudaMalloc(&dl, sizeof(double) * n * d * d));
+  if (e_bbt) CK(cudaMalloc(&de, sizeof(double) * n * d * d));
+  const int tb = 128;
+  const unsigned blocks = (unsigned)((n + tb - 1) / tb);
+  if (ds->storage == CV_STORE_F32)
+    materialize_kernel<float><<<blocks, tb, 0, ds->stream>>>((const float*)ds->x, (const float*)ds->D, ds->Vp, d, lo, n,
+                                                             ds->ctl, dm, dl, de);
+  else
+    materialize_kernel<double><<<blocks, tb, 0, ds->stream>>>((const double*)ds->x, (const double*)ds->D, ds->Vp, d, lo,
+                                                              n, ds->ctl, dm, dl, de);
+  CK(cudaGetLastError());
+  if (dm) CK(cudaMemcpyAsync(mu_beta, dm, sizeof(double) * n * d, cudaMemcpyDeviceToHost, ds->stream));
+  if (dl) CK(cudaMemcpyAsync(lam_beta, dl, sizeof(double) * n * d * d, cudaMemcpyDeviceToHost, ds->stream));
+  if (de) CK(cudaMemcpyAsync(e_bbt, de, sizeof(double) * n * d * d, cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  if (dm) CK(cudaFree(dm));
+  if (dl) CK(cudaFree(dl));
+  if (de) CK(cudaFree(de));
+  return CV_OK;
+}
+
+int32_t cv_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(CV_ERR_ARG, "bad host allocation");
+  CK(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
+  return CV_OK;
+}
+
+void cv_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int32_t warmup, int32_t sweeps,
+                        double* ms_total, double* ms_kernel, int32_t* launches) {
+  if (!ds || !st || !ms_total || !ms_kernel) return fail(CV_ERR_ARG, "null pointer");
+  if (sweeps < 1) return fail(CV_ERR_ARG, "sweeps must be >= 1");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  Ctl c;
+  reset_ctl(c);
+  c.cur = *st;
+  c.mode = MODE_SWEEP;
+  c.rel_tol = 0.0;  // the stop rule never fires: every timed sweep does the full pass
+  if ((rc = ctl_put(ds, c))) return rc;
+  derive_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
+  CK(cudaGetLastError());
+  for (int i = 0; i < warmup; ++i)
+    if ((rc = launch_pass(ds))) return rc;
+  CK(cudaStreamSynchronize(ds->stream));
+  std::vector<cudaEvent_t> evs(2 * (size_t)sweeps);
+  for (auto& e : evs) CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(ds->ev[0], ds->stream));
+  for (int i = 0; i < sweeps; ++i) {
+    CK(cudaEventRecord(evs[2 * i], ds->stream));
+    if ((rc = launch_pass(ds))) return rc;
+    CK(cudaEventRecord(evs[2 * i + 1], ds->stream));
+  }
+  CK(cudaEventRecord(ds->ev[1], ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, ds->ev[0], ds->ev[1]));
+  *ms_total = t;
+  double k = 0.0;
+  for (int i = 0; i < sweeps; ++i) {
+    CK(cudaEventElapsedTime(&t, evs[2 * i], evs[2 * i + 1]));
+    k += t;
+  }
+  *ms_kernel = k;
+  for (auto& e : evs) cudaEventDestroy(e);
+  if (launches) *launches = sweeps;
+  if ((rc = ctl_get(ds))) return rc;
+  if (ds->h_ctl->status != CV_OK) return state_status(ds->h_ctl->cur);
+  return CV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+// control.cuh -- one-thread kernels around the fused pass (setup, generator
+// hand-over, the multi-GPU tail).  Included by cavi.cu only.
+#pragma once
+
+#include "pass.cuh"
+
+namespace cavi {
+
+// One-CTA kernels around the pass --------------------------------------------
+__global__ void setup_kernel(Hyp* h) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) hyp_setup(*h);
+}
+
+// Generator of the next pass from ctl->cur (used after a host-provided state).
+__global__ void derive_kernel(const Hyp* h, Ctl* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) derive_pass(*h, *c);
+}
+
+// Set the generator of vb_init's state (K0, Lambda0, e_rho = 0).
+__global__ void init_gen_kernel(const Hyp* h, Ctl* c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int d = h->d;
+    for (int i = 0; i < d; ++i) c->pass.c[i] = h->K0[i];
+    for (int i = 0; i < d * d; ++i) {
+      c->pass.A[i] = h->L0[i];
+      c->pass.Ainv[i] = h->L0inv[i];
+    }
+    c->pass.lnA = h->lnL0;
+    c->pass.e_rho = 0.0;
+    c->mode = MODE_INIT;
+  }
+}
+
+// Set the generator of an arbitrary state's own moments (for vb_elbo of it).
+__global__ void state_gen_kernel(Ctl* c, int d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const cv_state& s = c->cur;
+    for (int i = 0; i < d; ++i) c->pass.c[i] = s.gen_c[i];
+    for (int i = 0; i < d * d; ++i) {
+      c->pass.A[i] = s.gen_A[i];
+      c->pass.Ainv[i] = s.gen_Ainv[i];
+    }
+    c->pass.lnA = s.gen_lnA;
+    c->pass.e_rho = s.gen_e_rho;
+  }
+}
+
+// Multi-GPU tail: pairwise tree over the gathered rank partials, then the tail.
+__global__ void tail_from_ranks_kernel(const Hyp* h, Ctl* c, const double* gathered, int world, int ns) {
+  __shared__ double s_tot[kMaxStats];
+  if (*(volatile const int*)&c->done) return;
+  const int tid = threadIdx.x;
+  if (tid < ns) {
+    double v[8];
+    for (int r = 0; r < world; ++r) v[r] = gathered[r * ns + tid];
+    for (int w = 1; w < world; w *= 2)
+      for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
+    s_tot[tid] = v[0];
+  }
+  __syncthreads();
+  if (tid == 0) tail(*h, *c, s_tot);
+}
+
+}  // namespace cavi

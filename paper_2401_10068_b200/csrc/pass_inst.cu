@@ -1,0 +1,16 @@
+// pass_inst.cu -- one explicit instantiation set of the fused pass per
+// dimension; the Makefile compiles this file once per CAVI_D in 1..15 so the
+// builds run in parallel.
+#include "pass.cuh"
+
+#ifndef CAVI_D
+#error "compile with -DCAVI_D=<1..15>"
+#endif
+
+#define CAVI_CAT2(a, b) a##b
+#define CAVI_CAT(a, b) CAVI_CAT2(a, b)
+
+cavi::PassFn CAVI_CAT(cavi_pass_d, CAVI_D)(int storage) {
+  return storage == CV_STORE_F32 ? (cavi::PassFn)cavi::pass_kernel<CAVI_D, float>
+                                 : (cavi::PassFn)cavi::pass_kernel<CAVI_D, double>;
+}
