@@ -594,6 +594,7 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
                        double* mu_beta, double* lam_beta, double* e_bbt) {
   if (!ds || !st) return fail(CV_ERR_ARG, "null pointer");
   if (lo < 0 || hi > ds->V || lo > hi) return fail(CV_ERR_ARG, "bad gene range");
+  if (st->d != ds->d) return fail(CV_ERR_ARG, "state does not belong to this dataset");
   (void)hp;
   const int64_t n = hi - lo;
   if (n == 0) return CV_OK;

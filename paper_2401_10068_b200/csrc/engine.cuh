@@ -334,6 +334,8 @@ static __device__ __noinline__ void tail(const Hyp& h, Ctl& c, const double* sta
   nw = c.cur;
   const Gen& gen = c.pass;
   nw.status = CV_OK;
+  nw.d = d;
+  nw.V = (int64_t)h.V;
   if (c.mode == MODE_INIT) {
     // vb_init (vb.py:82-111): globals at the prior; this pass measured the init moments.
     nw.n_iter = 0;

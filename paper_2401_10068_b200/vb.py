@@ -131,7 +131,9 @@ class VbState:
     # --- per-gene fields, materialised on demand
     def _materialise(self):
         if not self._lazy:
-            V, d = self._dds.V, self.dim
+            V, d = self._dds.V, self._dds.dim
+            if d != self.dim:
+                raise ValueError("state does not belong to this dataset")
             mu = np.empty((V, d))
             lam = np.empty((V, d, d))
             ebb = np.empty((V, d, d))
