@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--profile", action="store_true", help="under ncu: no clock soak, no e2e/cpu legs")
     p.add_argument("--converge", action="store_true", help="also time vb_fit to ELBO convergence")
     return p.parse_args()
 
@@ -212,7 +213,7 @@ def run_ours(args):
         _lib.check(_lib.lib().cv_bench_sweeps(dd.handle, C.byref(hs), C.byref(st._cs), args.warmup, args.steps,
                                               C.byref(ms_total), C.byref(ms_kernel), C.byref(nl)))
         # keep sampling clocks for >=1 s of the same sweeps if the timed region was shorter
-        soak = max(0, int(1000.0 / max(ms_total.value / args.steps, 1e-3)) - args.steps)
+        soak = 0 if args.profile else max(0, int(1000.0 / max(ms_total.value / args.steps, 1e-3)) - args.steps)
         if soak:
             a, b, c = C.c_double(), C.c_double(), C.c_int32()
             _lib.check(_lib.lib().cv_bench_sweeps(dd.handle, C.byref(hs), C.byref(st._cs), 0, min(soak, 20000),
@@ -247,10 +248,10 @@ def run_ours(args):
         s_conv, tr = vb.vb_fit(dd, hp, max_iter=100000, rel_tol=1e-8)
         line["converge"] = {"wall_s": time.time() - t, "iterations": len(tr), "final_elbo": float(tr.elbo[-1])}
 
-    if not args.no_e2e:
+    if not (args.no_e2e or args.profile):
         line["e2e"] = e2e(args, dd, hp)
     del dd
-    if not args.no_cpu:
+    if not (args.no_cpu or args.profile):
         sweep, Vs, sample = cpu_reference_sample(V, N, target_s=1.0)
         sweep()
         ts = [sweep() for _ in range(8)]

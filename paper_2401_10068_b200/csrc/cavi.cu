@@ -39,14 +39,14 @@ int fail(int code, const char* fmt, ...) {
 }  // namespace
 
 // one per dimension, from pass_inst.cu compiled with -DCAVI_D=1..15
-#define DECL(D) cavi::PassFn cavi_pass_d##D(int storage);
+#define DECL(D) cavi::PassKernel cavi_pass_d##D(int storage);
 DECL(1) DECL(2) DECL(3) DECL(4) DECL(5) DECL(6) DECL(7) DECL(8)
 DECL(9) DECL(10) DECL(11) DECL(12) DECL(13) DECL(14) DECL(15)
 #undef DECL
 
 namespace {
 
-PassFn pass_for(int d, int storage) {
+PassKernel pass_for(int d, int storage) {
   switch (d) {
 #define CASE(D) \
   case D:       \
@@ -55,7 +55,7 @@ PassFn pass_for(int d, int storage) {
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
     default:
-      return nullptr;
+      return PassKernel{nullptr, 0, 0};
   }
 }
 
@@ -81,7 +81,7 @@ struct cv_dataset {
   double* trace = nullptr;
   int trace_cap = 0;
   int grid = 0;
-  PassFn pass = nullptr;
+  PassKernel pass{nullptr, 0, 0};
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t graph = nullptr;
   int graph_unroll = 0;
@@ -141,10 +141,10 @@ int plan_and_alloc(cv_dataset* ds) {
   for (auto& e : ds->ev) CK(cudaEventCreate(&e));
   ds->device_bytes = nx * es * (1 + ds->d);
   ds->pass = pass_for(ds->d, ds->storage);
-  if (!ds->pass) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", ds->d, kMaxD);
+  if (!ds->pass.fn) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", ds->d, kMaxD);
   int dev_sms = 0, per_sm = 0;
   CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ds->device));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ds->pass, kThreads, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ds->pass.fn, ds->pass.threads, ds->pass.smem));
   ds->grid = (int)std::max<int64_t>(1, std::min<int64_t>(ds->n_chunks, (int64_t)dev_sms * std::max(per_sm, 1)));
   return CV_OK;
 }
@@ -168,12 +168,13 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.ctl = ds->ctl;
   a.hyp = ds->hyp;
   a.rank_out = rank_out;
+  a.l2_keep = ds->device_bytes < (size_t)64 << 20;
   return a;
 }
 
 int launch_pass(cv_dataset* ds) {
   if (ds->n_chunks == 0) return fail(CV_ERR_ARG, "empty shard");
-  ds->pass<<<ds->grid, kThreads, 0, ds->stream>>>(pass_args(ds, nullptr));
+  ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, nullptr));
   CK(cudaGetLastError());
   return CV_OK;
 }
@@ -268,7 +269,8 @@ int ensure_graph(cv_dataset* ds, int unroll) {
   ds->graph = nullptr;
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(ds->stream, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < unroll; ++i) ds->pass<<<ds->grid, kThreads, 0, ds->stream>>>(pass_args(ds, nullptr));
+  for (int i = 0; i < unroll; ++i)
+    ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, nullptr));
   cudaError_t e = cudaStreamEndCapture(ds->stream, &g);
   if (e != cudaSuccess) return fail(CV_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
   CK(cudaGraphInstantiate(&ds->graph, g, 0));

@@ -10,7 +10,17 @@
 #define CAVI_CAT2(a, b) a##b
 #define CAVI_CAT(a, b) CAVI_CAT2(a, b)
 
-cavi::PassFn CAVI_CAT(cavi_pass_d, CAVI_D)(int storage) {
-  return storage == CV_STORE_F32 ? (cavi::PassFn)cavi::pass_kernel<CAVI_D, float>
-                                 : (cavi::PassFn)cavi::pass_kernel<CAVI_D, double>;
+template <typename T>
+static cavi::PassKernel make_kernel() {
+  using G = cavi::Geometry<CAVI_D, T>;
+  cavi::PassKernel k;
+  k.fn = cavi::pass_kernel<CAVI_D, T>;
+  k.threads = cavi::kCtaThreads;
+  k.smem = G::kSmem;
+  cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
+  return k;
+}
+
+cavi::PassKernel CAVI_CAT(cavi_pass_d, CAVI_D)(int storage) {
+  return storage == CV_STORE_F32 ? make_kernel<float>() : make_kernel<double>();
 }
