@@ -13,7 +13,7 @@ __global__ void setup_kernel(Hyp* h) {
 
 // Generator of the next pass from ctl->cur (used after a host-provided state).
 __global__ void derive_kernel(const Hyp* h, Ctl* c) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) derive_pass(*h, *c);
+  if (threadIdx.x == 0 && blockIdx.x == 0) derive_pass_rt(*h, *c);
 }
 
 // Set the generator of vb_init's state (K0, Lambda0, e_rho = 0).
@@ -43,22 +43,6 @@ __global__ void state_gen_kernel(Ctl* c, int d) {
     c->pass.lnA = s.gen_lnA;
     c->pass.e_rho = s.gen_e_rho;
   }
-}
-
-// Multi-GPU tail: pairwise tree over the gathered rank partials, then the tail.
-__global__ void tail_from_ranks_kernel(const Hyp* h, Ctl* c, const double* gathered, int world, int ns) {
-  __shared__ double s_tot[kMaxStats];
-  if (*(volatile const int*)&c->done) return;
-  const int tid = threadIdx.x;
-  if (tid < ns) {
-    double v[8];
-    for (int r = 0; r < world; ++r) v[r] = gathered[r * ns + tid];
-    for (int w = 1; w < world; w *= 2)
-      for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
-    s_tot[tid] = v[0];
-  }
-  __syncthreads();
-  if (tid == 0) tail(*h, *c, s_tot);
 }
 
 }  // namespace cavi

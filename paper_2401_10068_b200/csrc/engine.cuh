@@ -9,6 +9,11 @@
 // reference vb.py:136-197 (the rho and (K, Lambda) blocks) and vb.py:216-304
 // (the bound) in the centred rank-1 form of SURVEY Appendix A, and the fit
 // loop's bookkeeping and stop rule (vb.py:307-347).
+//
+// The tail is templated on d and works in registers / the thread's stack and
+// in place on the control block: it sits on the critical path of every sweep
+// (a single thread runs it after the last chunk), so it must cost
+// microseconds, not a walk through global-memory scratch.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -21,10 +26,10 @@ namespace cavi {
 constexpr int kMaxD = CV_MAX_DIM;
 constexpr int kMaxD2 = CV_MAX_D2;
 constexpr int kMaxStats = kMaxD + kMaxD * (kMaxD + 1) / 2 + 2;  // 137
-constexpr int kChunk = 4096;         // genes per chunk (one CTA work unit)
+constexpr int kChunk = 4096;         // genes per chunk (one reduction unit)
 constexpr int kGroupChunks = 64;     // chunks per group
 constexpr int kOctants = 8;          // top of the reduction tree (GPU-count invariant)
-constexpr int kThreads = 256;        // threads per CTA of the pass
+constexpr int kThreads = 256;        // consumer threads per CTA of the pass
 constexpr int kWarps = kThreads / 32;
 
 constexpr double kLn2 = 0.69314718055994530942;
@@ -32,6 +37,8 @@ constexpr double kLnPi = 1.14472988584940017414;
 constexpr double kLn2Pi = 1.83787706640934548356;
 
 __host__ __device__ constexpr int n_stats(int d) { return d + d * (d + 1) / 2 + 2; }
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
 // Hyperparameters + sweep-invariant constants of the bound (reference model.py:126-151).
 struct Hyp {
@@ -49,6 +56,7 @@ struct Hyp {
   double dg_afit, lg_afit, dg_a0, lg_a0;
   double sum_dg_nu;  // sum_j digamma((nu + 1 - j)/2)   (vb.py:213)
   double mgl_nu;     // multigammaln(nu/2, d)
+  double ln_nu, ln_q0, ln_qv, ln_b0;
   int setup_status;
   double wL[kMaxD2], wJ[kMaxD2], wM[kMaxD2];  // setup workspace
 };
@@ -64,16 +72,8 @@ struct Gen {
 
 enum { MODE_INIT = 0, MODE_SWEEP = 1, MODE_ELBO = 2 };
 
-// Global-memory workspace of the (single-thread) tail: keeps the kernels' stack frames tiny.
-struct Scratch {
-  cv_state nw;
-  double G[kMaxD2], AG[kMaxD2], S[kMaxD2], L[kMaxD2], J[kMaxD2], M[kMaxD2];
-  double hv[kMaxD], dlt[kMaxD], k0c[kMaxD];
-};
-
 // Control block: current state, the generator of the next pass, fit loop control.
 struct Ctl {
-  Scratch scr;
   cv_state cur;
   Gen pass;
   double pend_a, pend_b;  // a_rho, b_rho of the state the next pass produces
@@ -94,7 +94,7 @@ struct Ctl {
 // ------------------------------------------------------------------ special functions
 static __device__ inline double digamma_pos(double x) {
   // x > 0: recurrence up to x >= 10, then the asymptotic series (error < 1e-16).
-  if (!(x > 0.0)) return __longlong_as_double(0x7ff8000000000000ULL);
+  if (!(x > 0.0)) return qnan();
   double acc = 0.0;
   while (x < 10.0) {
     acc -= 1.0 / x;
@@ -114,41 +114,106 @@ static __device__ inline double multigammaln(double a, int d) {
 }
 
 // ------------------------------------------------------------------ small dense SPD algebra
-// Row-major d x d, d <= 15.  Cholesky with the reference's jitter-once policy
+// Row-major D x D.  Cholesky with the reference's jitter-once policy
 // (linalg.py:279-298): on failure add 1e-10 * trace/d to the diagonal and retry.
-static __device__ __noinline__ bool chol(const double* A, double* L, int d) {
-  for (int i = 0; i < d * d; ++i) L[i] = 0.0;
-  for (int j = 0; j < d; ++j) {
-    double s = A[j * d + j];
-    for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+template <int D>
+__device__ __forceinline__ bool chol_t(const double* A, double* L) {
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) L[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    double s = A[j * D + j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s -= L[j * D + k] * L[j * D + k];
     if (!(s > 0.0)) return false;
     const double ljj = sqrt(s);
-    L[j * d + j] = ljj;
-    for (int i = j + 1; i < d; ++i) {
-      double t = A[i * d + j];
-      for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
-      L[i * d + j] = t / ljj;
+    const double rl = 1.0 / ljj;
+    L[j * D + j] = ljj;
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double t = A[i * D + j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= L[i * D + k] * L[j * D + k];
+      L[i * D + j] = t * rl;
     }
   }
   return true;
 }
 
-// inverse + log-determinant of an SPD matrix; returns false if not PD after the retry.
-// L, J, M: caller-provided d x d workspaces.
-static __device__ __noinline__ bool spd_inv_logdet(const double* A, double* Ainv, double* logdet, int d, double* L,
-                                            double* J, double* M) {
-  if (!chol(A, L, d)) {
+// inverse + log-determinant of an SPD matrix; false if not PD after the retry
+template <int D>
+__device__ __forceinline__ bool spd_inv_logdet_t(const double* A, double* Ainv, double* logdet) {
+  double L[D * D];
+  if (!chol_t<D>(A, L)) {
+    double tr = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) tr += A[j * D + j];
+    const double jit = 1e-10 * tr / D;
+    double J[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) J[i] = A[i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) J[j * D + j] += jit;
+    if (!chol_t<D>(J, L)) return false;
+  }
+  double prod = 1.0;
+  double M[D * D];  // L^-1, lower
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) M[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    prod *= L[j * D + j];
+    M[j * D + j] = 1.0 / L[j * D + j];
+#pragma unroll
+    for (int i = j + 1; i < D; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = j; k < i; ++k) t -= L[i * D + k] * M[k * D + j];
+      M[i * D + j] = t / L[i * D + i];
+    }
+  }
+  *logdet = 2.0 * log(prod);
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = i; j < D; ++j) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = j; k < D; ++k) t += M[k * D + i] * M[k * D + j];
+      Ainv[i * D + j] = t;
+      Ainv[j * D + i] = t;
+    }
+  return isfinite(*logdet);
+}
+
+// runtime-d variant, used once per call by the setup kernel (workspaces in Hyp)
+static __device__ __noinline__ bool spd_inv_logdet_rt(const double* A, double* Ainv, double* logdet, int d,
+                                                      double* L, double* J, double* M) {
+  auto chol = [&](const double* X) {
+    for (int i = 0; i < d * d; ++i) L[i] = 0.0;
+    for (int j = 0; j < d; ++j) {
+      double s = X[j * d + j];
+      for (int k = 0; k < j; ++k) s -= L[j * d + k] * L[j * d + k];
+      if (!(s > 0.0)) return false;
+      L[j * d + j] = sqrt(s);
+      for (int i = j + 1; i < d; ++i) {
+        double t = X[i * d + j];
+        for (int k = 0; k < j; ++k) t -= L[i * d + k] * L[j * d + k];
+        L[i * d + j] = t / L[j * d + j];
+      }
+    }
+    return true;
+  };
+  if (!chol(A)) {
     double tr = 0.0;
     for (int j = 0; j < d; ++j) tr += A[j * d + j];
-    const double jit = 1e-10 * tr / d;
     for (int i = 0; i < d * d; ++i) J[i] = A[i];
-    for (int j = 0; j < d; ++j) J[j * d + j] += jit;
-    if (!chol(J, L, d)) return false;
+    for (int j = 0; j < d; ++j) J[j * d + j] += 1e-10 * tr / d;
+    if (!chol(J)) return false;
   }
   double ld = 0.0;
   for (int j = 0; j < d; ++j) ld += log(L[j * d + j]);
   *logdet = 2.0 * ld;
-  // M = L^-1 (lower), then A^-1 = M^T M
   for (int i = 0; i < d * d; ++i) M[i] = 0.0;
   for (int j = 0; j < d; ++j) {
     M[j * d + j] = 1.0 / L[j * d + j];
@@ -168,10 +233,12 @@ static __device__ __noinline__ bool spd_inv_logdet(const double* A, double* Ainv
   return true;
 }
 
-static __device__ inline double rel_delta(const double* nw, const double* old, int n) {
+template <int N>
+__device__ __forceinline__ double rel_delta_t(const double* nw, const double* old) {
   // reference vb.py:307-309
   double mo = 0.0, md = 0.0;
-  for (int i = 0; i < n; ++i) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
     mo = fmax(mo, fabs(old[i]));
     const double df = fabs(nw[i] - old[i]);
     md = (df > md || df != df) ? df : md;
@@ -183,7 +250,7 @@ static __device__ inline double rel_delta(const double* nw, const double* old, i
 static __device__ __noinline__ void hyp_setup(Hyp& h) {
   const int d = h.d;
   h.setup_status = CV_OK;
-  if (!spd_inv_logdet(h.L0, h.L0inv, &h.lnL0, d, h.wL, h.wJ, h.wM)) {
+  if (!spd_inv_logdet_rt(h.L0, h.L0inv, &h.lnL0, d, h.wL, h.wJ, h.wM)) {
     h.setup_status = CV_ERR_NUMERIC;
     return;
   }
@@ -194,6 +261,10 @@ static __device__ __noinline__ void hyp_setup(Hyp& h) {
   h.lg_afit = lgamma(h.a_fit);
   h.dg_a0 = digamma_pos(h.a0);
   h.lg_a0 = lgamma(h.a0);
+  h.ln_nu = log(h.nu);
+  h.ln_q0 = log(h.q0);
+  h.ln_qv = log(h.qv);
+  h.ln_b0 = log(h.b0);
   h.proper_q = h.nu > d - 1;
   h.sum_dg_nu = 0.0;
   h.mgl_nu = 0.0;
@@ -207,248 +278,301 @@ static __device__ __noinline__ void hyp_setup(Hyp& h) {
 }
 
 // ------------------------------------------------------------------ the bound
-// vb_elbo (reference vb.py:216-304) of state `st`, whose per-gene moments come
-// from generator `gen`, from the pass statistics of that generator.
-static __device__ __noinline__ double elbo_of(const Hyp& h, const cv_state& st, const Gen& gen, const double* stats,
-                                       int* status, Scratch& w) {
-  const int d = h.d;
+// vb_elbo (reference vb.py:216-304) of the state (a, b, k0k, S = lam0l_inv^-1,
+// ln|lam0l_inv|), whose per-gene moments come from generator `gen`, from the
+// pass statistics of that generator.
+template <int D>
+__device__ __forceinline__ double elbo_t(const Hyp& h, double a, double b, const double* k0k, const double* S,
+                                         double ln_det_l, const Gen& gen, const double* stats, int* status) {
   if (!h.proper_q) {
     *status = CV_ERR_IMPROPER;
-    return __longlong_as_double(0x7ff8000000000000ULL);
+    return qnan();
   }
+  constexpr int NS = n_stats(D);
   const double V = h.V, nu = h.nu, qv = h.qv;
-  const double* g = stats;
-  const double R = stats[n_stats(d) - 2];
-  const double Ld = stats[n_stats(d) - 1];
-  double* G = w.G;
+  const double R = stats[NS - 2];
+  const double Ld = stats[NS - 1];
+  double G[D * D], Ai[D * D];
   {
-    int p = d;
-    for (int j = 0; j < d; ++j)
-      for (int k = j; k < d; ++k) {
-        G[j * d + k] = stats[p];
-        G[k * d + j] = stats[p];
+    int p = D;
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+#pragma unroll
+      for (int k = j; k < D; ++k) {
+        G[j * D + k] = stats[p];
+        G[k * D + j] = stats[p];
         ++p;
       }
   }
-  double* S = w.S;
-  double lnL;
-  if (!spd_inv_logdet(st.lam0l_inv, S, &lnL, d, w.L, w.J, w.M)) {
-    *status = CV_ERR_NUMERIC;
-    return __longlong_as_double(0x7ff8000000000000ULL);
-  }
-  const double ln_s = -st.ln_det_lam0l_inv;
-  const double a = st.a_rho, b = st.b_rho;
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) Ai[i] = gen.Ainv[i];
+  const double ln_s = -ln_det_l;
   const double dga = (a == h.a_fit) ? h.dg_afit : (a == h.a0 ? h.dg_a0 : digamma_pos(a));
   const double lga = (a == h.a_fit) ? h.lg_afit : (a == h.a0 ? h.lg_a0 : lgamma(a));
   const double e_rho = a / b;
   const double lnb = log(b);
   const double e_lnrho = dga - lnb;
-  const double e_lnlam = h.sum_dg_nu + d * kLn2 + ln_s;
-  // h_ = Ainv g, dlt = k0k - c
-  double* hv = w.hv;
-  double* dlt = w.dlt;
-  for (int i = 0; i < d; ++i) {
+  const double e_lnlam = h.sum_dg_nu + D * kLn2 + ln_s;
+  // hv = Ainv g, dlt = k0k - c
+  double hv[D], dlt[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
     double t = 0.0;
-    for (int j = 0; j < d; ++j) t += gen.Ainv[i * d + j] * g[j];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
     hv[i] = t;
-    dlt[i] = st.k0k[i] - gen.c[i];
+    dlt[i] = k0k[i] - gen.c[i];
   }
-  // T = Ainv G Ainv ; scatter = V Ainv + T - dlt h^T - h dlt^T + V dlt dlt^T ; tr(S scatter)
-  double* AG = w.AG;
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) {
+  // scatter = V Ainv + Ainv G Ainv - dlt h^T - h dlt^T + V dlt dlt^T ; tr(S scatter)
+  double AG[D * D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
       double t = 0.0;
-      for (int k = 0; k < d; ++k) t += gen.Ainv[i * d + k] * G[k * d + j];
-      AG[i * d + j] = t;
+#pragma unroll
+      for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
+      AG[i * D + j] = t;
     }
-  double tr1 = 0.0;
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) {
+  double tr1 = 0.0, quad = 0.0, tr0 = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
       double T = 0.0;
-      for (int k = 0; k < d; ++k) T += AG[i * d + k] * gen.Ainv[k * d + j];
-      const double sc = V * gen.Ainv[i * d + j] + T - dlt[i] * hv[j] - hv[i] * dlt[j] + V * dlt[i] * dlt[j];
-      tr1 += S[i * d + j] * sc;
+#pragma unroll
+      for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
+      const double sc = V * Ai[i * D + j] + T - dlt[i] * hv[j] - hv[i] * dlt[j] + V * dlt[i] * dlt[j];
+      const double sij = S[i * D + j];
+      tr1 += sij * sc;
+      quad += (k0k[i] - h.K0[i]) * sij * (k0k[j] - h.K0[j]);
+      tr0 += h.L0inv[j * D + i] * sij;
     }
-  double quad = 0.0, tr0 = 0.0;
-  for (int i = 0; i < d; ++i) {
-    const double dki = st.k0k[i] - h.K0[i];
-    for (int j = 0; j < d; ++j) {
-      quad += dki * S[i * d + j] * (st.k0k[j] - h.K0[j]);
-      tr0 += h.L0inv[i * d + j] * S[j * d + i];
-    }
-  }
   const double ldsig = -(V * gen.lnA + Ld);
   const double t_lik = 0.5 * V * (e_lnrho - kLn2Pi) - 0.5 * e_rho * R;
-  const double t_beta = 0.5 * V * e_lnlam - 0.5 * V * d * kLn2Pi - 0.5 * (nu * tr1 + V * d / qv);
-  const double t_k = 0.5 * d * log(h.q0) - 0.5 * d * kLn2Pi + 0.5 * e_lnlam - 0.5 * h.q0 * (nu * quad + d / qv);
-  double t_lam = 0.5 * (h.n0 - d - 1) * e_lnlam - 0.5 * nu * tr0;
+  const double t_beta = 0.5 * V * e_lnlam - 0.5 * V * D * kLn2Pi - 0.5 * (nu * tr1 + V * D / qv);
+  const double t_k = 0.5 * D * h.ln_q0 - 0.5 * D * kLn2Pi + 0.5 * e_lnlam - 0.5 * h.q0 * (nu * quad + D / qv);
+  double t_lam = 0.5 * (h.n0 - D - 1) * e_lnlam - 0.5 * nu * tr0;
   if (h.has_zprior) t_lam -= h.zprior;
-  const double t_rho = h.a0 * log(h.b0) - h.lg_a0 + (h.a0 - 1.0) * e_lnrho - h.b0 * e_rho;
-  const double h_beta = 0.5 * ldsig + 0.5 * V * d * (1.0 + kLn2Pi);
+  const double t_rho = h.a0 * h.ln_b0 - h.lg_a0 + (h.a0 - 1.0) * e_lnrho - h.b0 * e_rho;
+  const double h_beta = 0.5 * ldsig + 0.5 * V * D * (1.0 + kLn2Pi);
   const double h_rho = a - lnb + lga + (1.0 - a) * dga;
-  const double e_lnq_k = 0.5 * d * log(qv) - 0.5 * d * kLn2Pi + 0.5 * e_lnlam - 0.5 * d;
-  const double z_q = 0.5 * nu * d * kLn2 + 0.5 * nu * ln_s + h.mgl_nu;
-  const double e_lnq_lam = 0.5 * (nu - d - 1) * e_lnlam - 0.5 * nu * d - z_q;
+  const double e_lnq_k = 0.5 * D * h.ln_qv - 0.5 * D * kLn2Pi + 0.5 * e_lnlam - 0.5 * D;
+  const double z_q = 0.5 * nu * D * kLn2 + 0.5 * nu * ln_s + h.mgl_nu;
+  const double e_lnq_lam = 0.5 * (nu - D - 1) * e_lnlam - 0.5 * nu * D - z_q;
   *status = CV_OK;
   return t_lik + t_beta + t_k + t_lam + t_rho + h_beta + h_rho - e_lnq_k - e_lnq_lam;
 }
 
 // generator of the next pass from the current state (vb.py:136-144)
-static __device__ inline void derive_pass(const Hyp& h, Ctl& c) {
-  const int d = h.d;
-  const cv_state& s = c.cur;
-  for (int i = 0; i < d; ++i) c.pass.c[i] = s.k0k[i];
-  for (int i = 0; i < d * d; ++i) {
+template <int D>
+__device__ __forceinline__ void derive_pass_t(const Hyp& h, Ctl& c) {
+  cv_state& s = c.cur;
+  const double rnu = 1.0 / h.nu;
+#pragma unroll
+  for (int i = 0; i < D; ++i) c.pass.c[i] = s.k0k[i];
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
     c.pass.A[i] = s.e_lam[i];
-    c.pass.Ainv[i] = s.lam0l_inv[i] / h.nu;
+    c.pass.Ainv[i] = s.lam0l_inv[i] * rnu;
   }
-  c.pass.lnA = d * log(h.nu) - s.ln_det_lam0l_inv;
+  c.pass.lnA = D * h.ln_nu - s.ln_det_lam0l_inv;
   c.pend_a = h.a_fit;
   c.pend_b = h.b0 + 0.5 * s.resid;
   c.pass.e_rho = c.pend_a / c.pend_b;
 }
 
-static __device__ inline void copy_gen_to_state(const Gen& g, cv_state& s, int d) {
-  for (int i = 0; i < d; ++i) s.gen_c[i] = g.c[i];
+// runtime-d generator derivation (after a host-provided state)
+static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
+  const int d = h.d;
+  cv_state& s = c.cur;
+  for (int i = 0; i < d; ++i) c.pass.c[i] = s.k0k[i];
   for (int i = 0; i < d * d; ++i) {
-    s.gen_A[i] = g.A[i];
-    s.gen_Ainv[i] = g.Ainv[i];
+    c.pass.A[i] = s.e_lam[i];
+    c.pass.Ainv[i] = s.lam0l_inv[i] / h.nu;
   }
-  s.gen_lnA = g.lnA;
-  s.gen_e_rho = g.e_rho;
+  c.pass.lnA = d * h.ln_nu - s.ln_det_lam0l_inv;
+  c.pend_a = h.a_fit;
+  c.pend_b = h.b0 + 0.5 * s.resid;
+  c.pass.e_rho = c.pend_a / c.pend_b;
 }
 
-// The tail: new state from the pass statistics; trace, stop rule, next generator.
-static __device__ __noinline__ void tail(const Hyp& h, Ctl& c, const double* stats) {
-  const int d = h.d;
-  const int ns = n_stats(d);
+// The tail: new state (in place in c.cur) from the pass statistics; trace, stop rule, next generator.
+template <int D>
+__device__ __noinline__ void tail_t(const Hyp& h, Ctl& c, const double* stats) {
+  constexpr int NS = n_stats(D);
+  cv_state& s = c.cur;
+  const Gen& gen = c.pass;
   if (c.mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
-    int es;
-    c.cur.elbo = elbo_of(h, c.cur, c.pass, stats, &es, c.scr);
-    c.cur.elbo_status = es;
+    double S[D * D], L[D * D], ld;
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) L[i] = s.lam0l_inv[i];
+    int es = CV_ERR_NUMERIC;
+    double e = qnan();
+    if (spd_inv_logdet_t<D>(L, S, &ld)) e = elbo_t<D>(h, s.a_rho, s.b_rho, s.k0k, S, s.ln_det_lam0l_inv, gen, stats, &es);
+    s.elbo = e;
+    s.elbo_status = es;
     return;
   }
   bool finite = true;
-  for (int i = 0; i < ns; ++i) finite = finite && isfinite(stats[i]);
-  cv_state& nw = c.scr.nw;
-  nw = c.cur;
-  const Gen& gen = c.pass;
-  nw.status = CV_OK;
-  nw.d = d;
-  nw.V = (int64_t)h.V;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) finite = finite && isfinite(stats[i]);
+  // previous values needed by the parameter deltas
+  double k_old[D], l_old[D * D];
+  const double e_rho_old = s.e_rho;
+#pragma unroll
+  for (int i = 0; i < D; ++i) k_old[i] = s.k0k[i];
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) l_old[i] = s.lam0l_inv[i];
+
+  double k_new[D], L[D * D], S[D * D], ld = 0.0;
+  int status = CV_OK;
+  double a, b, e_rho;
   if (c.mode == MODE_INIT) {
     // vb_init (vb.py:82-111): globals at the prior; this pass measured the init moments.
-    nw.n_iter = 0;
-    nw.a_rho = h.a0;
-    nw.b_rho = h.b0;
-    nw.e_rho = h.a0 / h.b0;
-    for (int i = 0; i < d; ++i) nw.k0k[i] = h.K0[i];
-    for (int i = 0; i < d * d; ++i) {
-      nw.lam0l_inv[i] = h.L0[i];
-      nw.e_lam[i] = h.nu * h.L0inv[i];
+    a = h.a0;
+    b = h.b0;
+    e_rho = h.a0 / h.b0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) k_new[i] = h.K0[i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) {
+      L[i] = h.L0[i];
+      S[i] = h.L0inv[i];
     }
-    nw.ln_det_lam0l_inv = h.lnL0;
+    ld = h.lnL0;
   } else {
     // (K, Lambda) block, centred (vb.py:172-183):
     //   dlt = (Ainv g + q0 (K0 - c)) / qv ; k0k = c + dlt
     //   lam0l_inv = L0inv + V Ainv + Ainv G Ainv + q0 (K0-c)(K0-c)^T - qv dlt dlt^T
-    const double* g = stats;
-    double* G = c.scr.G;
-    int p = d;
-    for (int j = 0; j < d; ++j)
-      for (int k = j; k < d; ++k) {
-        G[j * d + k] = stats[p];
-        G[k * d + j] = stats[p];
-        ++p;
-      }
-    double* k0c = c.scr.k0c;
-    double* dlt = c.scr.dlt;
-    for (int i = 0; i < d; ++i) {
+    double G[D * D], Ai[D * D];
+    {
+      int p = D;
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int k = j; k < D; ++k) {
+          G[j * D + k] = stats[p];
+          G[k * D + j] = stats[p];
+          ++p;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) Ai[i] = gen.Ainv[i];
+    double k0c[D], dlt[D];
+    const double rqv = 1.0 / h.qv;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
       double t = 0.0;
-      for (int j = 0; j < d; ++j) t += gen.Ainv[i * d + j] * g[j];
+#pragma unroll
+      for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
       k0c[i] = h.K0[i] - gen.c[i];
-      dlt[i] = (t + h.q0 * k0c[i]) / h.qv;
-      nw.k0k[i] = gen.c[i] + dlt[i];
+      dlt[i] = (t + h.q0 * k0c[i]) * rqv;
+      k_new[i] = gen.c[i] + dlt[i];
     }
-    double* AG = c.scr.AG;
-    for (int i = 0; i < d; ++i)
-      for (int j = 0; j < d; ++j) {
+    double AG[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
         double t = 0.0;
-        for (int k = 0; k < d; ++k) t += gen.Ainv[i * d + k] * G[k * d + j];
-        AG[i * d + j] = t;
+#pragma unroll
+        for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
+        AG[i * D + j] = t;
       }
-    for (int i = 0; i < d; ++i)
-      for (int j = i; j < d; ++j) {
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = i; j < D; ++j) {
         double T = 0.0;
-        for (int k = 0; k < d; ++k) T += AG[i * d + k] * gen.Ainv[k * d + j];
-        const double v = h.L0inv[i * d + j] + h.V * gen.Ainv[i * d + j] + T + h.q0 * k0c[i] * k0c[j] -
-                         h.qv * dlt[i] * dlt[j];
-        nw.lam0l_inv[i * d + j] = v;
-        nw.lam0l_inv[j * d + i] = v;
+#pragma unroll
+        for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
+        const double v =
+            h.L0inv[i * D + j] + h.V * Ai[i * D + j] + T + h.q0 * k0c[i] * k0c[j] - h.qv * dlt[i] * dlt[j];
+        L[i * D + j] = v;
+        L[j * D + i] = v;
       }
-    double* S = c.scr.S;
-    double ld;
-    if (!finite) {
-      nw.status = CV_ERR_NUMERIC;
-    } else if (!spd_inv_logdet(nw.lam0l_inv, S, &ld, d, c.scr.L, c.scr.J, c.scr.M)) {
-      nw.status = CV_ERR_NUMERIC;  // "Q(Lambda) rate inversion failed after jitter retry"
-    } else {
-      nw.ln_det_lam0l_inv = ld;
-      for (int i = 0; i < d * d; ++i) nw.e_lam[i] = h.nu * S[i];
-    }
-    nw.a_rho = c.pend_a;
-    nw.b_rho = c.pend_b;
-    nw.e_rho = gen.e_rho;
-    nw.n_iter = c.cur.n_iter + 1;
+    if (!finite || !spd_inv_logdet_t<D>(L, S, &ld)) status = CV_ERR_NUMERIC;  // rate inversion failed
+    a = c.pend_a;
+    b = c.pend_b;
+    e_rho = gen.e_rho;
   }
-  for (int i = 0; i < d; ++i) {
+  // write the new state in place
+  s.status = status;
+  s.d = D;
+  s.V = (int64_t)h.V;
+  s.a_rho = a;
+  s.b_rho = b;
+  s.e_rho = e_rho;
+#pragma unroll
+  for (int i = 0; i < D; ++i) s.k0k[i] = k_new[i];
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
+    s.lam0l_inv[i] = L[i];
+    s.e_lam[i] = h.nu * S[i];
+  }
+  s.ln_det_lam0l_inv = ld;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
     double t = 0.0;
-    for (int j = 0; j < d; ++j) t += nw.e_lam[i * d + j] * nw.k0k[j];
-    nw.e_lamk[i] = t;
+#pragma unroll
+    for (int j = 0; j < D; ++j) t += h.nu * S[i * D + j] * k_new[j];
+    s.e_lamk[i] = t;
+    s.gen_c[i] = gen.c[i];
   }
-  copy_gen_to_state(gen, nw, d);
-  nw.resid = stats[ns - 2];
-  nw.elbo = __longlong_as_double(0x7ff8000000000000ULL);
-  nw.elbo_status = CV_OK;
-  if (nw.status == CV_OK && (c.compute_elbo || c.mode == MODE_INIT)) {
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) {
+    s.gen_A[i] = gen.A[i];
+    s.gen_Ainv[i] = gen.Ainv[i];
+  }
+  s.gen_lnA = gen.lnA;
+  s.gen_e_rho = gen.e_rho;
+  s.resid = stats[NS - 2];
+  s.elbo = qnan();
+  s.elbo_status = CV_OK;
+  if (status == CV_OK && (c.compute_elbo || c.mode == MODE_INIT)) {
     int es;
-    nw.elbo = elbo_of(h, nw, gen, stats, &es, c.scr);
-    nw.elbo_status = es;
+    s.elbo = elbo_t<D>(h, a, b, k_new, S, ld, gen, stats, &es);
+    s.elbo_status = es;
   }
-  if (c.mode == MODE_SWEEP && nw.status == CV_OK) {
-    // fit bookkeeping (vb.py:332-347)
-    const double dk = rel_delta(nw.k0k, c.cur.k0k, d);
-    const double dr = rel_delta(&nw.e_rho, &c.cur.e_rho, 1);
-    const double dl = rel_delta(nw.lam0l_inv, c.cur.lam0l_inv, d * d);
-    const int it = c.iter;
-    if (it < c.tr_cap) {
-      c.tr_dk[it] = dk;
-      c.tr_drho[it] = dr;
-      c.tr_dlam[it] = dl;
-      c.tr_elbo[it] = c.compute_elbo ? nw.elbo : __longlong_as_double(0x7ff8000000000000ULL);
-    }
-    c.iter = it + 1;
-    if (c.compute_elbo) {
-      if (nw.elbo_status != CV_OK) {
-        c.status = nw.elbo_status;
-        c.done = 1;
-      } else {
-        if (c.have_prev && fabs(nw.elbo - c.prev_elbo) < c.rel_tol * fabs(nw.elbo)) c.done = 1;
-        c.prev_elbo = nw.elbo;
-        c.have_prev = 1;
+  if (c.mode == MODE_SWEEP) {
+    s.n_iter = s.n_iter + 1;
+    if (status == CV_OK) {
+      // fit bookkeeping (vb.py:332-347)
+      const double dk = rel_delta_t<D>(k_new, k_old);
+      const double dr = rel_delta_t<1>(&e_rho, &e_rho_old);
+      const double dl = rel_delta_t<D * D>(L, l_old);
+      const int it = c.iter;
+      if (it < c.tr_cap) {
+        c.tr_dk[it] = dk;
+        c.tr_drho[it] = dr;
+        c.tr_dlam[it] = dl;
+        c.tr_elbo[it] = c.compute_elbo ? s.elbo : qnan();
       }
-    } else if (fmax(dk, fmax(dr, dl)) < c.param_tol) {
-      c.done = 1;
+      c.iter = it + 1;
+      if (c.compute_elbo) {
+        if (s.elbo_status != CV_OK) {
+          c.status = s.elbo_status;
+          c.done = 1;
+        } else {
+          if (c.have_prev && fabs(s.elbo - c.prev_elbo) < c.rel_tol * fabs(s.elbo)) c.done = 1;
+          c.prev_elbo = s.elbo;
+          c.have_prev = 1;
+        }
+      } else if (fmax(dk, fmax(dr, dl)) < c.param_tol) {
+        c.done = 1;
+      }
+      if (c.iter >= c.max_iter) c.done = 1;
     }
-    if (c.iter >= c.max_iter) c.done = 1;
+  } else {
+    s.n_iter = 0;
   }
-  if (nw.status != CV_OK) {
-    c.status = nw.status;
+  if (status != CV_OK) {
+    c.status = status;
     c.done = 1;
   }
-  c.cur = nw;
   c.mode = MODE_SWEEP;
-  if (nw.status == CV_OK) derive_pass(h, c);
+  if (status == CV_OK) derive_pass_t<D>(h, c);
 }
 
 }  // namespace cavi

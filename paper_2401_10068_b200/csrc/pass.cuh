@@ -132,14 +132,18 @@ __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const dou
 
 // Sum of the group's chunk partials (index order) / octants (index order) / pairwise tree.
 // Executed by the `nthr` consumer threads (tid in [0, nthr)), synchronised on named barrier 1.
-template <int NS>
+template <int D>
 __device__ void finish_group_and_maybe_tail(const PassArgs& a, int64_t grp, double* s_tot, int* s_flag, int tid,
                                             int nthr) {
+  constexpr int NS = n_stats(D);
   const int64_t c0 = grp * kGroupChunks;
   const int64_t c1 = lmin(c0 + kGroupChunks, a.n_chunks);
   if (tid < NS) {
     double s = 0.0;
-    for (int64_t c = c0; c < c1; ++c) s += __ldcg(a.partials + c * NS + tid);
+    const int n = (int)(c1 - c0);
+#pragma unroll 8
+    for (int i = 0; i < kGroupChunks; ++i)
+      if (i < n) s += __ldcg(a.partials + (c0 + i) * NS + tid);
     a.gpartials[grp * NS + tid] = s;
   }
   __threadfence();
@@ -160,6 +164,7 @@ __device__ void finish_group_and_maybe_tail(const PassArgs& a, int64_t grp, doub
       const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
       const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
       double s = 0.0;
+#pragma unroll 8
       for (int64_t gg = g0; gg < g1; ++gg) s += __ldcg(a.gpartials + (gg - a.group_lo) * NS + tid);
       oct[o] = s;
     }
@@ -173,12 +178,12 @@ __device__ void finish_group_and_maybe_tail(const PassArgs& a, int64_t grp, doub
   if (a.rank_out) {
     if (tid < NS) a.rank_out[tid] = s_tot[tid];
   } else if (tid == 0) {
-    tail(*a.hyp, *a.ctl, s_tot);
+    tail_t<D>(*a.hyp, *a.ctl, s_tot);
   }
 }
 
 // chunk partial (fixed-order block reduction) -> partials[chunk]; group / final bookkeeping
-template <int NS, int NWARPS>
+template <int D, int NWARPS, int NS = n_stats(D)>
 __device__ __forceinline__ void publish_chunk(const PassArgs& a, int64_t chunk, double (&acc)[NS],
                                               double (*s_warp)[NS], double* s_tot, int* s_flag, int tid) {
   const int lane = tid & 31, warp = tid >> 5;
@@ -208,7 +213,7 @@ __device__ __forceinline__ void publish_chunk(const PassArgs& a, int64_t chunk, 
   ptx::bar_sync(1, NTHR);
   if (*s_flag) {
     __threadfence();
-    finish_group_and_maybe_tail<NS>(a, grp, s_tot, s_flag, tid, NTHR);
+    finish_group_and_maybe_tail<D>(a, grp, s_tot, s_flag, tid, NTHR);
   }
   ptx::bar_sync(1, NTHR);
 }
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
       }
     }
     acc[NS - 1] = lg.log_value();
-    publish_chunk<NS, kWarps>(a, chunk, acc, s_warp, s_tot, &s_flag, tid);
+    publish_chunk<D, kWarps>(a, chunk, acc, s_warp, s_tot, &s_flag, tid);
   }
 }
 
