@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,7 +75,10 @@ struct cv_dataset {
   int oct_lo = 0, oct_hi = kOctants;
   double* partials = nullptr;
   double* gpartials = nullptr;
-  unsigned int* counters = nullptr;  // [n_groups] + gdone
+  unsigned int* counters = nullptr;  // [n_groups] gcount | [8] ocount | odone
+  unsigned long long* ticket = nullptr;
+  double* opartials = nullptr;
+  int n_live_octants = 0;
   int* flags = nullptr;              // [0] bad input bits, [1] scratch status
   Ctl* ctl = nullptr;
   Hyp* hyp = nullptr;
@@ -88,6 +92,7 @@ struct cv_dataset {
   Ctl* h_ctl = nullptr;  // pinned mirror
   int bad_input = 0;
   size_t device_bytes = 0;
+  unsigned long long* cta_trace = nullptr;  // CAVI_TRACE_CTA diagnostics
 };
 
 namespace {
@@ -131,8 +136,18 @@ int plan_and_alloc(cv_dataset* ds) {
   CK(cudaMalloc(&ds->D, nx * es * ds->d));
   CK(cudaMalloc(&ds->partials, sizeof(double) * ns * std::max<int64_t>(ds->n_chunks, 1)));
   CK(cudaMalloc(&ds->gpartials, sizeof(double) * ns * std::max<int64_t>(ds->n_groups, 1)));
-  CK(cudaMalloc(&ds->counters, sizeof(unsigned int) * (ds->n_groups + 1)));
-  CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + 1), ds->stream));
+  CK(cudaMalloc(&ds->counters, sizeof(unsigned int) * (ds->n_groups + kOctants + 1)));
+  CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + kOctants + 1), ds->stream));
+  CK(cudaMalloc(&ds->ticket, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(ds->ticket, 0, sizeof(unsigned long long), ds->stream));
+  CK(cudaMalloc(&ds->opartials, sizeof(double) * ns * kOctants));
+  ds->n_live_octants = 0;
+  for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
+    const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
+    const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
+                                         ds->group_lo + ds->n_groups);
+    if (h1 > h0) ++ds->n_live_octants;
+  }
   CK(cudaMalloc(&ds->flags, sizeof(int) * 4));
   CK(cudaMemsetAsync(ds->flags, 0, sizeof(int) * 4, ds->stream));
   CK(cudaMalloc(&ds->ctl, sizeof(Ctl)));
@@ -164,10 +179,15 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.partials = ds->partials;
   a.gpartials = ds->gpartials;
   a.gcount = ds->counters;
-  a.gdone = ds->counters + ds->n_groups;
+  a.ocount = ds->counters + ds->n_groups;
+  a.odone = ds->counters + ds->n_groups + kOctants;
+  a.opartials = ds->opartials;
+  a.ticket = ds->ticket;
+  a.n_live_octants = ds->n_live_octants;
   a.ctl = ds->ctl;
   a.hyp = ds->hyp;
   a.rank_out = rank_out;
+  a.cta_trace = ds->cta_trace;
   a.l2_keep = ds->device_bytes < (size_t)64 << 20;
   return a;
 }
@@ -329,7 +349,8 @@ void cv_dataset_destroy(cv_dataset* ds) {
   cudaSetDevice(ds->device);
   if (ds->stream) cudaStreamSynchronize(ds->stream);
   if (ds->graph) cudaGraphExecDestroy(ds->graph);
-  void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters,
+  void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters, ds->ticket,
+                  ds->opartials,
                   ds->flags, ds->ctl, ds->hyp, ds->trace};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -666,6 +687,22 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   }
   CK(cudaEventRecord(ds->ev[1], ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
+  if (const char* path = getenv("CAVI_TRACE_CTA")) {
+    // diagnostics: one more sweep with per-CTA globaltimer stamps, dumped as text
+    CK(cudaMalloc(&ds->cta_trace, sizeof(unsigned long long) * 4 * ds->grid));
+    CK(cudaMemsetAsync(ds->cta_trace, 0, sizeof(unsigned long long) * 4 * ds->grid, ds->stream));
+    if ((rc = launch_pass(ds))) return rc;
+    std::vector<unsigned long long> tr(4 * (size_t)ds->grid);
+    CK(cudaMemcpyAsync(tr.data(), ds->cta_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaStreamSynchronize(ds->stream));
+    CK(cudaFree(ds->cta_trace));
+    ds->cta_trace = nullptr;
+    if (FILE* f = fopen(path, "w")) {
+      for (int b = 0; b < ds->grid; ++b)
+        fprintf(f, "%d %llu %llu %llu %llu\n", b, tr[4 * b], tr[4 * b + 1], tr[4 * b + 2], tr[4 * b + 3]);
+      fclose(f);
+    }
+  }
   float t = 0.f;
   CK(cudaEventElapsedTime(&t, ds->ev[0], ds->ev[1]));
   *ms_total = t;

@@ -41,11 +41,16 @@ struct PassArgs {
   int l2_keep;             // stream fits in L2: keep it resident across sweeps
   double* partials;        // [n_chunks][ns]
   double* gpartials;       // [n_groups][ns]
-  unsigned int* gcount;    // [n_groups]
-  unsigned int* gdone;     // [1]
+  unsigned int* gcount;    // [n_groups] arrivals per group
+  unsigned int* ocount;    // [8] arrivals per octant
+  unsigned int* odone;     // [1] completed octants
+  double* opartials;       // [8][ns]
+  unsigned long long* ticket;  // chunk tickets (monotone across sweeps)
+  int n_live_octants;      // octants of this shard holding at least one group
   Ctl* ctl;
   const Hyp* hyp;
   double* rank_out;        // multi-GPU: [ns] subtree partial of this shard; null -> run the tail
+  unsigned long long* cta_trace;  // optional [grid][4] globaltimer stamps (diagnostics)
 };
 
 typedef void (*PassFn)(PassArgs);
@@ -55,6 +60,17 @@ struct PassKernel {
   int threads;
   int smem;  // dynamic shared memory bytes
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned int smid() {
+  unsigned int r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 
 __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
@@ -130,95 +146,84 @@ __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const dou
   return den;
 }
 
-// Sum of the group's chunk partials (index order) / octants (index order) / pairwise tree.
-// Executed by the `nthr` consumer threads (tid in [0, nthr)), synchronised on named barrier 1.
-template <int D>
-__device__ void finish_group_and_maybe_tail(const PassArgs& a, int64_t grp, double* s_tot, int* s_flag, int tid,
-                                            int nthr) {
-  constexpr int NS = n_stats(D);
-  const int64_t c0 = grp * kGroupChunks;
-  const int64_t c1 = lmin(c0 + kGroupChunks, a.n_chunks);
-  if (tid < NS) {
+// ---------------------------------------------------------------- deterministic reduction
+// Every level sums its children in index order, so the totals are bit-identical
+// whichever CTA / warp / GPU computed a chunk.  The level that completes a
+// parent (a per-parent arrival counter reaching its child count) computes it;
+// nobody waits for anybody.  Warp-level code: lane l handles statistics
+// l, l+32, ...
+
+// sum_{i<n} src[i*NS + stat] for this lane's stats, index order, loads pipelined
+template <int NS>
+__device__ __forceinline__ void warp_sum_rows(const double* src, int64_t n, double* dst, int lane) {
+  for (int st = lane; st < NS; st += 32) {
     double s = 0.0;
-    const int n = (int)(c1 - c0);
 #pragma unroll 8
-    for (int i = 0; i < kGroupChunks; ++i)
-      if (i < n) s += __ldcg(a.partials + (c0 + i) * NS + tid);
-    a.gpartials[grp * NS + tid] = s;
+    for (int64_t i = 0; i < n; ++i) s += __ldcg(src + i * NS + st);
+    dst[st] = s;
   }
-  __threadfence();
-  ptx::bar_sync(1, nthr);
-  if (tid == 0) {
-    a.gcount[grp] = 0u;  // ready for the next sweep
-    const unsigned int prev = atomicAdd(a.gdone, 1u);
-    *s_flag = (prev == (unsigned int)(a.n_groups - 1));
+}
+
+// lane 0 publishes (fence, cumulative over the warp's stores) and counts an arrival
+__device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned int need, int lane) {
+  unsigned int last = 0;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == need - 1;
+    if (last) __threadfence();
   }
-  ptx::bar_sync(1, nthr);
-  if (!*s_flag) return;
-  __threadfence();
-  if (tid < NS) {
-    double oct[kOctants];
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+// chunk partial -> group -> octant -> total (-> tail), by whichever warp completes each level
+template <int D, int NS = n_stats(D)>
+__device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, double* s_tot,
+                                          int lane) {
+  for (int st = lane; st < NS; st += 32) a.partials[chunk * NS + st] = chunk_sum[st];
+  const int64_t grp = chunk / kGroupChunks;
+  const int64_t c0 = grp * kGroupChunks;
+  const int64_t nc = lmin(c0 + kGroupChunks, a.n_chunks) - c0;
+  if (!warp_arrive_last(a.gcount + grp, (unsigned int)nc, lane)) return;
+  // group complete
+  if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
+  warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.gpartials + grp * NS, lane);
+  const int64_t gg = a.group_lo + grp;  // global group index
+  const int o = (int)(gg / a.groups_per_octant);
+  const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
+  const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
+  if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
+  // octant complete
+  if (lane == 0) a.ocount[o] = 0u;
+  warp_sum_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, a.opartials + o * NS, lane);
+  if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
+  // every octant this shard owns is complete: pairwise tree over them (empty octants add 0)
+  if (lane == 0) *a.odone = 0u;
+  for (int st = lane; st < NS; st += 32) {
+    double v[kOctants];
 #pragma unroll
-    for (int o = 0; o < kOctants; ++o) oct[o] = 0.0;
-    for (int o = a.oct_lo; o < a.oct_hi; ++o) {
-      const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
-      const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
-      double s = 0.0;
-#pragma unroll 8
-      for (int64_t gg = g0; gg < g1; ++gg) s += __ldcg(a.gpartials + (gg - a.group_lo) * NS + tid);
-      oct[o] = s;
+    for (int q = 0; q < kOctants; ++q) v[q] = 0.0;
+    for (int q = a.oct_lo; q < a.oct_hi; ++q) {
+      const int64_t h0 = lmax((int64_t)q * a.groups_per_octant, a.group_lo);
+      const int64_t h1 = lmin(lmin((int64_t)(q + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
+      if (h1 > h0) v[q] = __ldcg(a.opartials + q * NS + st);
     }
-    // pairwise tree over the owned octants (a power-of-two aligned span)
     for (int w = 1; w < a.oct_hi - a.oct_lo; w *= 2)
-      for (int o = a.oct_lo; o + w < a.oct_hi; o += 2 * w) oct[o] = oct[o] + oct[o + w];
-    s_tot[tid] = oct[a.oct_lo];
+      for (int q = a.oct_lo; q + w < a.oct_hi; q += 2 * w) v[q] = v[q] + v[q + w];
+    s_tot[st] = v[a.oct_lo];
+    if (a.rank_out) a.rank_out[st] = v[a.oct_lo];
   }
-  if (tid == 0) *a.gdone = 0u;
-  ptx::bar_sync(1, nthr);
+  __syncwarp();
   if (a.rank_out) {
-    if (tid < NS) a.rank_out[tid] = s_tot[tid];
-  } else if (tid == 0) {
+    if (lane == 0) __threadfence();
+  } else if (lane == 0) {
     tail_t<D>(*a.hyp, *a.ctl, s_tot);
   }
 }
 
-// chunk partial (fixed-order block reduction) -> partials[chunk]; group / final bookkeeping
-template <int D, int NWARPS, int NS = n_stats(D)>
-__device__ __forceinline__ void publish_chunk(const PassArgs& a, int64_t chunk, double (&acc)[NS],
-                                              double (*s_warp)[NS], double* s_tot, int* s_flag, int tid) {
-  const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NTHR = NWARPS * 32;
-#pragma unroll
-  for (int i = 0; i < NS; ++i) {
-    double v = acc[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) s_warp[warp][i] = v;
-  }
-  ptx::bar_sync(1, NTHR);
-  if (tid < NS) {
-    double s = s_warp[0][tid];
-#pragma unroll
-    for (int w = 1; w < NWARPS; ++w) s += s_warp[w][tid];
-    a.partials[chunk * NS + tid] = s;
-  }
-  __threadfence();
-  ptx::bar_sync(1, NTHR);
-  const int64_t grp = chunk / kGroupChunks;
-  if (tid == 0) {
-    const unsigned int need = (unsigned int)(lmin((grp + 1) * kGroupChunks, a.n_chunks) - grp * kGroupChunks);
-    const unsigned int prev = atomicAdd(a.gcount + grp, 1u);
-    *s_flag = (prev == need - 1);
-  }
-  ptx::bar_sync(1, NTHR);
-  if (*s_flag) {
-    __threadfence();
-    finish_group_and_maybe_tail<D>(a, grp, s_tot, s_flag, tid, NTHR);
-  }
-  ptx::bar_sync(1, NTHR);
-}
-
 // ---------------------------------------------------------------- pipeline geometry
+constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles < kSlots chunks)
+
 template <int D, typename T>
 struct Geometry {
   static constexpr int kTile = D <= 3 ? 1024 : (D <= 7 ? 512 : 256);  // genes per stage
@@ -226,10 +231,18 @@ struct Geometry {
   static constexpr int kGenesPerThread = kTile / kThreads;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
   static constexpr uint32_t kStageBytes = kColBytes * (1 + D);
-  static constexpr int kStages = (196608 / kStageBytes) > 8 ? 8 : (196608 / kStageBytes);
-  static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
+  static constexpr int kNS = n_stats(D);
+  static constexpr int kSlotBytes = kSlots * kWarps * kNS * 8;
+  static constexpr int kBudget = 200 * 1024 - kSlotBytes;
+  static constexpr int kStages = (kBudget / (int)kStageBytes) > 8 ? 8 : (kBudget / (int)kStageBytes);
+  // [stages][1+D][tile] | full[stages] | empty[stages] | stage chunk id[stages] | slots
+  static constexpr int kOffBar = kStages * kStageBytes;
+  static constexpr int kOffChunk = kOffBar + 2 * kStages * 8;
+  static constexpr int kOffSlots = kOffChunk + kStages * 8;
+  static constexpr int kSmem = kOffSlots + kSlotBytes;
   static_assert(kStages >= 2, "stage too large");
   static_assert(kTile % kThreads == 0, "tile must split evenly across consumers");
+  static_assert(kStages <= (kSlots - 1) * kTilesPerChunk, "warp drift could lap the reduction slots");
 };
 
 constexpr int kProducerWarp = kWarps;       // warp index of the TMA producer
@@ -240,61 +253,80 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
   using G = Geometry<D, T>;
   constexpr int NS = n_stats(D);
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_warp[kWarps][NS];
-  __shared__ double s_tot[NS];
-  __shared__ int s_flag;
+  __shared__ double s_red[kWarps][NS];  // per-warp chunk sum / final totals
+  __shared__ unsigned int s_cnt[kSlots];
   T* stage_base = reinterpret_cast<T*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::kStages * G::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::kOffBar);
   uint64_t* empty = full + G::kStages;
+  int64_t* stage_chunk = reinterpret_cast<int64_t*>(smem + G::kOffChunk);
+  double* slots = reinterpret_cast<double*>(smem + G::kOffSlots);  // [kSlots][kWarps][NS]
 
   const Ctl* ctl = a.ctl;
   if (*(volatile const int*)&ctl->done) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < G::kStages; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], kWarps);
+    for (int q = 0; q < G::kStages; ++q) {
+      ptx::mbar_init(&full[q], 1);
+      ptx::mbar_init(&empty[q], kWarps);
     }
+    for (int q = 0; q < kSlots; ++q) s_cnt[q] = 0u;
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 4] = globaltimer_ns();
 
   if (warp == kProducerWarp) {
-    // ---------------- TMA producer: one elected lane streams every tile of this CTA's chunks
+    // ---------------- TMA producer: takes chunk tickets (dynamic load balance) and streams
+    // each chunk tile by tile into the stage ring; a -1 chunk id ends the consumers.
     if (lane == 0) {
       const T* xs = static_cast<const T*>(a.x);
       const T* Ds = static_cast<const T*>(a.D);
       const uint64_t pol = a.l2_keep ? ptx::policy_evict_last() : ptx::policy_evict_first();
+      const unsigned long long period = (unsigned long long)a.n_chunks + gridDim.x;  // tickets per sweep
       int stage = 0;
       uint32_t parity = 1;  // fresh "empty" barriers count as released
-      for (int64_t chunk = blockIdx.x; chunk < a.n_chunks; chunk += gridDim.x) {
-        for (int t = 0; t < G::kTilesPerChunk; ++t) {
+      for (;;) {
+        const int64_t chunk = (int64_t)(atomicAdd(a.ticket, 1ull) % period);
+        const bool end = chunk >= a.n_chunks;
+        for (int t = 0; t < (end ? 1 : G::kTilesPerChunk); ++t) {
           ptx::mbar_wait(&empty[stage], parity);
-          ptx::mbar_arrive_expect_tx(&full[stage], G::kStageBytes);
-          const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
-          T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
-          ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
+          if (end) {
+            stage_chunk[stage] = -1;
+            ptx::mbar_arrive(&full[stage]);
+          } else {
+            stage_chunk[stage] = chunk;
+            ptx::mbar_arrive_expect_tx(&full[stage], G::kStageBytes);
+            const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
+            T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
+            ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
 #pragma unroll
-          for (int j = 0; j < D; ++j)
-            ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kTile, Ds + (int64_t)j * a.Vp + g0, G::kColBytes, &full[stage],
-                          pol);
+            for (int j = 0; j < D; ++j)
+              ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kTile, Ds + (int64_t)j * a.Vp + g0, G::kColBytes, &full[stage],
+                            pol);
+          }
           if (++stage == G::kStages) {
             stage = 0;
             parity ^= 1u;
           }
         }
+        if (end) break;
       }
+      if (a.cta_trace) a.cta_trace[blockIdx.x * 4 + 1] = globaltimer_ns();
     }
-    return;  // consumers synchronise on named barrier 1 only
+    return;
   }
 
-  // ---------------- consumers
+  // ---------------- consumers: 8 independent warps, no CTA barrier in the steady state
   GeneCoef<D> k;
   load_coef<D>(k, ctl->pass);
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
   uint32_t parity = 0;
-  for (int64_t chunk = blockIdx.x; chunk < a.n_chunks; chunk += gridDim.x) {
+  int n_done = 0;
+  for (;;) {
+    ptx::mbar_wait(&full[stage], parity);
+    const int64_t chunk = stage_chunk[stage];
+    if (chunk < 0) break;
     double acc[NS];
 #pragma unroll
     for (int i = 0; i < NS; ++i) acc[i] = 0.0;
@@ -302,7 +334,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
     lg.init();
 #pragma unroll 1
     for (int t = 0; t < G::kTilesPerChunk; ++t) {
-      ptx::mbar_wait(&full[stage], parity);
+      if (t) ptx::mbar_wait(&full[stage], parity);
       const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
       double prod = 1.0;
 #pragma unroll
@@ -322,7 +354,42 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
       }
     }
     acc[NS - 1] = lg.log_value();
-    publish_chunk<D, kWarps>(a, chunk, acc, s_warp, s_tot, &s_flag, tid);
+    // warp sum (fixed butterfly) -> this warp's slot of the chunk
+    double* slot = slots + (size_t)(n_done % kSlots) * kWarps * NS;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      double v = acc[i];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == (i & 31)) slot[warp * NS + i] = v;
+    }
+    // the last warp to finish the chunk sums the 8 warp slots (warp order) and carries on up
+    unsigned int last = 0;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&s_cnt[n_done % kSlots], 1u) == kWarps - 1;
+      if (last) {
+        s_cnt[n_done % kSlots] = 0u;
+        __threadfence_block();
+      }
+    }
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      double* mine = s_red[warp];
+      for (int st = lane; st < NS; st += 32) {
+        double v = slot[st];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) v += slot[w * NS + st];
+        mine[st] = v;
+      }
+      __syncwarp();
+      finish_chunk<D>(a, chunk, mine, mine, lane);
+    }
+    ++n_done;
+  }
+  if (a.cta_trace && tid == 0) {
+    a.cta_trace[blockIdx.x * 4 + 2] = globaltimer_ns();
+    a.cta_trace[blockIdx.x * 4 + 3] = smid();
   }
 }
 
