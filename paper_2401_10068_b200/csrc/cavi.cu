@@ -689,17 +689,18 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   CK(cudaStreamSynchronize(ds->stream));
   if (const char* path = getenv("CAVI_TRACE_CTA")) {
     // diagnostics: one more sweep with per-CTA globaltimer stamps, dumped as text
-    CK(cudaMalloc(&ds->cta_trace, sizeof(unsigned long long) * 4 * ds->grid));
-    CK(cudaMemsetAsync(ds->cta_trace, 0, sizeof(unsigned long long) * 4 * ds->grid, ds->stream));
+    CK(cudaMalloc(&ds->cta_trace, sizeof(unsigned long long) * 8 * ds->grid));
+    CK(cudaMemsetAsync(ds->cta_trace, 0, sizeof(unsigned long long) * 8 * ds->grid, ds->stream));
     if ((rc = launch_pass(ds))) return rc;
-    std::vector<unsigned long long> tr(4 * (size_t)ds->grid);
+    std::vector<unsigned long long> tr(8 * (size_t)ds->grid);
     CK(cudaMemcpyAsync(tr.data(), ds->cta_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, ds->stream));
     CK(cudaStreamSynchronize(ds->stream));
     CK(cudaFree(ds->cta_trace));
     ds->cta_trace = nullptr;
     if (FILE* f = fopen(path, "w")) {
       for (int b = 0; b < ds->grid; ++b)
-        fprintf(f, "%d %llu %llu %llu %llu\n", b, tr[4 * b], tr[4 * b + 1], tr[4 * b + 2], tr[4 * b + 3]);
+        fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu\n", b, tr[8 * b], tr[8 * b + 1], tr[8 * b + 2], tr[8 * b + 3],
+                tr[8 * b + 4], tr[8 * b + 5], tr[8 * b + 6]);
       fclose(f);
     }
   }

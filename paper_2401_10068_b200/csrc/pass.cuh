@@ -50,7 +50,7 @@ struct PassArgs {
   Ctl* ctl;
   const Hyp* hyp;
   double* rank_out;        // multi-GPU: [ns] subtree partial of this shard; null -> run the tail
-  unsigned long long* cta_trace;  // optional [grid][4] globaltimer stamps (diagnostics)
+  unsigned long long* cta_trace;  // optional [grid][8] globaltimer stamps (diagnostics)
 };
 
 typedef void (*PassFn)(PassArgs);
@@ -180,6 +180,7 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
 template <int D, int NS = n_stats(D)>
 __device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, double* s_tot,
                                           int lane) {
+  const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) a.partials[chunk * NS + st] = chunk_sum[st];
   const int64_t grp = chunk / kGroupChunks;
   const int64_t c0 = grp * kGroupChunks;
@@ -199,6 +200,10 @@ __device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, cons
   if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
   // every octant this shard owns is complete: pairwise tree over them (empty octants add 0)
   if (lane == 0) *a.odone = 0u;
+  if (a.cta_trace && lane == 0) {
+    a.cta_trace[blockIdx.x * 8 + 4] = t_entry;
+    a.cta_trace[blockIdx.x * 8 + 5] = globaltimer_ns();
+  }
   for (int st = lane; st < NS; st += 32) {
     double v[kOctants];
 #pragma unroll
@@ -219,6 +224,7 @@ __device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, cons
   } else if (lane == 0) {
     tail_t<D>(*a.hyp, *a.ctl, s_tot);
   }
+  if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------- pipeline geometry
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
     ptx::fence_mbar_init();
   }
   __syncthreads();
-  if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 4] = globaltimer_ns();
+  if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 8] = globaltimer_ns();
 
   if (warp == kProducerWarp) {
     // ---------------- TMA producer: takes chunk tickets (dynamic load balance) and streams
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
         }
         if (end) break;
       }
-      if (a.cta_trace) a.cta_trace[blockIdx.x * 4 + 1] = globaltimer_ns();
+      if (a.cta_trace) a.cta_trace[blockIdx.x * 8 + 1] = globaltimer_ns();
     }
     return;
   }
@@ -388,8 +394,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
     ++n_done;
   }
   if (a.cta_trace && tid == 0) {
-    a.cta_trace[blockIdx.x * 4 + 2] = globaltimer_ns();
-    a.cta_trace[blockIdx.x * 4 + 3] = smid();
+    a.cta_trace[blockIdx.x * 8 + 2] = globaltimer_ns();
+    a.cta_trace[blockIdx.x * 8 + 3] = smid();
   }
 }
 
