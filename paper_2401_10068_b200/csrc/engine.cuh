@@ -277,13 +277,55 @@ static __device__ __noinline__ void hyp_setup(Hyp& h) {
   if (h.has_zprior) h.zprior = 0.5 * h.n0 * d * kLn2 + 0.5 * h.n0 * h.lnL0 + multigammaln(0.5 * h.n0, d);
 }
 
+// Register/stack copy of the hyperparameters a d-specialised tail needs, loaded in
+// one burst of independent loads (the tail is latency-bound: one thread, end of sweep).
+template <int D>
+struct HypT {
+  int n0, has_zprior, proper_q;
+  double a0, b0, q0, V, nu, qv, lnL0, zprior, a_fit, dg_afit, lg_afit, dg_a0, lg_a0, sum_dg_nu, mgl_nu;
+  double ln_nu, ln_q0, ln_qv, ln_b0;
+  double K0[D], L0[D * D], L0inv[D * D];
+  __device__ __forceinline__ void load(const Hyp& __restrict__ h) {
+    n0 = h.n0;
+    has_zprior = h.has_zprior;
+    proper_q = h.proper_q;
+    a0 = h.a0; b0 = h.b0; q0 = h.q0; V = h.V; nu = h.nu; qv = h.qv; lnL0 = h.lnL0; zprior = h.zprior;
+    a_fit = h.a_fit; dg_afit = h.dg_afit; lg_afit = h.lg_afit; dg_a0 = h.dg_a0; lg_a0 = h.lg_a0;
+    sum_dg_nu = h.sum_dg_nu; mgl_nu = h.mgl_nu; ln_nu = h.ln_nu; ln_q0 = h.ln_q0; ln_qv = h.ln_qv; ln_b0 = h.ln_b0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) K0[i] = h.K0[i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) {
+      L0[i] = h.L0[i];
+      L0inv[i] = h.L0inv[i];
+    }
+  }
+};
+
+// the generator a pass streamed against, in registers
+template <int D>
+struct GenT {
+  double c[D], A[D * D], Ainv[D * D], lnA, e_rho;
+  __device__ __forceinline__ void load(const Gen& __restrict__ g) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) c[i] = g.c[i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) {
+      A[i] = g.A[i];
+      Ainv[i] = g.Ainv[i];
+    }
+    lnA = g.lnA;
+    e_rho = g.e_rho;
+  }
+};
+
 // ------------------------------------------------------------------ the bound
 // vb_elbo (reference vb.py:216-304) of the state (a, b, k0k, S = lam0l_inv^-1,
 // ln|lam0l_inv|), whose per-gene moments come from generator `gen`, from the
 // pass statistics of that generator.
 template <int D>
-__device__ __forceinline__ double elbo_t(const Hyp& h, double a, double b, const double* k0k, const double* S,
-                                         double ln_det_l, const Gen& gen, const double* stats, int* status) {
+__device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, const double* k0k, const double* S,
+                                         double ln_det_l, const GenT<D>& gen, const double* stats, int* status) {
   if (!h.proper_q) {
     *status = CV_ERR_IMPROPER;
     return qnan();
@@ -366,7 +408,7 @@ __device__ __forceinline__ double elbo_t(const Hyp& h, double a, double b, const
 
 // generator of the next pass from the current state (vb.py:136-144)
 template <int D>
-__device__ __forceinline__ void derive_pass_t(const Hyp& h, Ctl& c) {
+__device__ __forceinline__ void derive_pass_t(const HypT<D>& h, Ctl& c) {
   cv_state& s = c.cur;
   const double rnu = 1.0 / h.nu;
 #pragma unroll
@@ -399,10 +441,13 @@ static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
 
 // The tail: new state (in place in c.cur) from the pass statistics; trace, stop rule, next generator.
 template <int D>
-__device__ __noinline__ void tail_t(const Hyp& h, Ctl& c, const double* stats) {
+__device__ __noinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
   constexpr int NS = n_stats(D);
+  HypT<D> h;
+  h.load(hyp);
+  GenT<D> gen;
+  gen.load(c.pass);
   cv_state& s = c.cur;
-  const Gen& gen = c.pass;
   if (c.mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
     double S[D * D], L[D * D], ld;
 #pragma unroll

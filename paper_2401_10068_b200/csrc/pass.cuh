@@ -158,8 +158,13 @@ template <int NS>
 __device__ __forceinline__ void warp_sum_rows(const double* src, int64_t n, double* dst, int lane) {
   for (int st = lane; st < NS; st += 32) {
     double s = 0.0;
-#pragma unroll 8
-    for (int64_t i = 0; i < n; ++i) s += __ldcg(src + i * NS + st);
+    for (int64_t i0 = 0; i0 < n; i0 += 16) {
+      double v[16];  // 16 independent loads in flight, then added in index order (+0.0 past the end)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = (i0 + j < n) ? __ldcg(src + (i0 + j) * NS + st) : 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) s += v[j];
+    }
     dst[st] = s;
   }
 }
@@ -232,13 +237,18 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 
 template <int D, typename T>
 struct Geometry {
+  // consumer warps: 16 where the per-gene state fits ~100 registers, 8 for large d
+  static constexpr int kCons = D <= 7 ? 512 : 256;
+  static constexpr int kCWarps = kCons / 32;
+  static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
+  static constexpr int kProducerWarp = kCWarps;
   static constexpr int kTile = D <= 3 ? 1024 : (D <= 7 ? 512 : 256);  // genes per stage
   static constexpr int kTilesPerChunk = kChunk / kTile;
-  static constexpr int kGenesPerThread = kTile / kThreads;  // consumer genes per stage
+  static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
   static constexpr uint32_t kStageBytes = kColBytes * (1 + D);
   static constexpr int kNS = n_stats(D);
-  static constexpr int kSlotBytes = kSlots * kWarps * kNS * 8;
+  static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   static constexpr int kBudget = 200 * 1024 - kSlotBytes;
   static constexpr int kStages = (kBudget / (int)kStageBytes) > 8 ? 8 : (kBudget / (int)kStageBytes);
   // [stages][1+D][tile] | full[stages] | empty[stages] | stage chunk id[stages] | slots
@@ -247,17 +257,17 @@ struct Geometry {
   static constexpr int kOffSlots = kOffChunk + kStages * 8;
   static constexpr int kSmem = kOffSlots + kSlotBytes;
   static_assert(kStages >= 2, "stage too large");
-  static_assert(kTile % kThreads == 0, "tile must split evenly across consumers");
+  static_assert(kTile % kCons == 0, "tile must split evenly across consumers");
   static_assert(kStages <= (kSlots - 1) * kTilesPerChunk, "warp drift could lap the reduction slots");
 };
 
-constexpr int kProducerWarp = kWarps;       // warp index of the TMA producer
-constexpr int kCtaThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
-
 template <int D, typename T>
-__global__ void __launch_bounds__(kCtaThreads, 1) pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, 1) pass_kernel(PassArgs a) {
   using G = Geometry<D, T>;
   constexpr int NS = n_stats(D);
+  constexpr int kWarps = G::kCWarps;
+  constexpr int kThreads = G::kCons;
+  constexpr int kProducerWarp = G::kProducerWarp;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_red[kWarps][NS];  // per-warp chunk sum / final totals
   __shared__ unsigned int s_cnt[kSlots];

@@ -15,7 +15,7 @@ static cavi::PassKernel make_kernel() {
   using G = cavi::Geometry<CAVI_D, T>;
   cavi::PassKernel k;
   k.fn = cavi::pass_kernel<CAVI_D, T>;
-  k.threads = cavi::kCtaThreads;
+  k.threads = G::kCtaThreads;
   k.smem = G::kSmem;
   cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   return k;
