@@ -428,52 +428,67 @@ __device__ __forceinline__ void derive_pass_t(const HypT<D>& h, Ctl& c) {
 static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
   const int d = h.d;
   cv_state& s = c.cur;
+  const double rnu = 1.0 / h.nu;  // same arithmetic as tail_t's hand-over
   for (int i = 0; i < d; ++i) c.pass.c[i] = s.k0k[i];
   for (int i = 0; i < d * d; ++i) {
     c.pass.A[i] = s.e_lam[i];
-    c.pass.Ainv[i] = s.lam0l_inv[i] / h.nu;
+    c.pass.Ainv[i] = s.lam0l_inv[i] * rnu;
   }
   c.pass.lnA = d * h.ln_nu - s.ln_det_lam0l_inv;
   c.pend_a = h.a_fit;
   c.pend_b = h.b0 + 0.5 * s.resid;
-  c.pass.e_rho = c.pend_a / c.pend_b;
+  c.pass.e_rho = h.a_fit / c.pend_b;
 }
 
-// The tail: new state (in place in c.cur) from the pass statistics; trace, stop rule, next generator.
+// The tail: new state (in place in c.cur) from the pass statistics; trace, stop rule,
+// next generator.  Structured as load-everything / compute in registers / store-everything:
+// a single thread runs it at the end of every sweep, so its dependent global round trips
+// (not its flops) are what the sweep pays for.
 template <int D>
 __device__ __noinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
   constexpr int NS = n_stats(D);
+  // ---- loads (independent, issued back to back)
   HypT<D> h;
   h.load(hyp);
   GenT<D> gen;
   gen.load(c.pass);
   cv_state& s = c.cur;
-  if (c.mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
-    double S[D * D], L[D * D], ld;
+  const int mode = c.mode, compute_elbo = c.compute_elbo, have_prev = c.have_prev, iter = c.iter;
+  const int max_iter = c.max_iter, tr_cap = c.tr_cap, n_iter_old = s.n_iter;
+  const double prev_elbo = c.prev_elbo, rel_tol = c.rel_tol, param_tol = c.param_tol;
+  const double pend_a = c.pend_a, pend_b = c.pend_b;
+  double* tr_elbo = c.tr_elbo;
+  double* tr_dk = c.tr_dk;
+  double* tr_drho = c.tr_drho;
+  double* tr_dlam = c.tr_dlam;
+  double st[NS];
 #pragma unroll
-    for (int i = 0; i < D * D; ++i) L[i] = s.lam0l_inv[i];
+  for (int i = 0; i < NS; ++i) st[i] = stats[i];
+  double k_old[D], l_old[D * D];
+  const double e_rho_old = s.e_rho, a_old = s.a_rho, b_old = s.b_rho, ld_old = s.ln_det_lam0l_inv;
+#pragma unroll
+  for (int i = 0; i < D; ++i) k_old[i] = s.k0k[i];
+#pragma unroll
+  for (int i = 0; i < D * D; ++i) l_old[i] = s.lam0l_inv[i];
+
+  if (mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
+    double S[D * D], ld;
     int es = CV_ERR_NUMERIC;
     double e = qnan();
-    if (spd_inv_logdet_t<D>(L, S, &ld)) e = elbo_t<D>(h, s.a_rho, s.b_rho, s.k0k, S, s.ln_det_lam0l_inv, gen, stats, &es);
+    if (spd_inv_logdet_t<D>(l_old, S, &ld)) e = elbo_t<D>(h, a_old, b_old, k_old, S, ld_old, gen, st, &es);
     s.elbo = e;
     s.elbo_status = es;
     return;
   }
   bool finite = true;
 #pragma unroll
-  for (int i = 0; i < NS; ++i) finite = finite && isfinite(stats[i]);
-  // previous values needed by the parameter deltas
-  double k_old[D], l_old[D * D];
-  const double e_rho_old = s.e_rho;
-#pragma unroll
-  for (int i = 0; i < D; ++i) k_old[i] = s.k0k[i];
-#pragma unroll
-  for (int i = 0; i < D * D; ++i) l_old[i] = s.lam0l_inv[i];
+  for (int i = 0; i < NS; ++i) finite = finite && isfinite(st[i]);
 
+  // ---- compute
   double k_new[D], L[D * D], S[D * D], ld = 0.0;
   int status = CV_OK;
   double a, b, e_rho;
-  if (c.mode == MODE_INIT) {
+  if (mode == MODE_INIT) {
     // vb_init (vb.py:82-111): globals at the prior; this pass measured the init moments.
     a = h.a0;
     b = h.b0;
@@ -490,27 +505,26 @@ __device__ __noinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats)
     // (K, Lambda) block, centred (vb.py:172-183):
     //   dlt = (Ainv g + q0 (K0 - c)) / qv ; k0k = c + dlt
     //   lam0l_inv = L0inv + V Ainv + Ainv G Ainv + q0 (K0-c)(K0-c)^T - qv dlt dlt^T
-    double G[D * D], Ai[D * D];
+    double G[D * D];
     {
       int p = D;
 #pragma unroll
       for (int j = 0; j < D; ++j)
 #pragma unroll
         for (int k = j; k < D; ++k) {
-          G[j * D + k] = stats[p];
-          G[k * D + j] = stats[p];
+          G[j * D + k] = st[p];
+          G[k * D + j] = st[p];
           ++p;
         }
     }
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) Ai[i] = gen.Ainv[i];
+    const double* Ai = gen.Ainv;
     double k0c[D], dlt[D];
     const double rqv = 1.0 / h.qv;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       double t = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
+      for (int j = 0; j < D; ++j) t += Ai[i * D + j] * st[j];
       k0c[i] = h.K0[i] - gen.c[i];
       dlt[i] = (t + h.q0 * k0c[i]) * rqv;
       k_new[i] = gen.c[i] + dlt[i];
@@ -538,86 +552,104 @@ __device__ __noinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats)
         L[j * D + i] = v;
       }
     if (!finite || !spd_inv_logdet_t<D>(L, S, &ld)) status = CV_ERR_NUMERIC;  // rate inversion failed
-    a = c.pend_a;
-    b = c.pend_b;
+    a = pend_a;
+    b = pend_b;
     e_rho = gen.e_rho;
   }
-  // write the new state in place
-  s.status = status;
-  s.d = D;
-  s.V = (int64_t)h.V;
-  s.a_rho = a;
-  s.b_rho = b;
-  s.e_rho = e_rho;
-#pragma unroll
-  for (int i = 0; i < D; ++i) s.k0k[i] = k_new[i];
-#pragma unroll
-  for (int i = 0; i < D * D; ++i) {
-    s.lam0l_inv[i] = L[i];
-    s.e_lam[i] = h.nu * S[i];
-  }
-  s.ln_det_lam0l_inv = ld;
+  double elbo = qnan();
+  int elbo_status = CV_OK;
+  if (status == CV_OK && (compute_elbo || mode == MODE_INIT)) elbo = elbo_t<D>(h, a, b, k_new, S, ld, gen, st, &elbo_status);
+  double elamk[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) {
     double t = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) t += h.nu * S[i * D + j] * k_new[j];
-    s.e_lamk[i] = t;
+    elamk[i] = t;
+  }
+  // fit bookkeeping (vb.py:332-347)
+  int done = 0, c_status = CV_OK, new_iter = iter, new_have_prev = have_prev;
+  double new_prev = prev_elbo, dk = 0.0, dr = 0.0, dl = 0.0;
+  const bool sweep_ok = mode == MODE_SWEEP && status == CV_OK;
+  if (sweep_ok) {
+    dk = rel_delta_t<D>(k_new, k_old);
+    dr = rel_delta_t<1>(&e_rho, &e_rho_old);
+    dl = rel_delta_t<D * D>(L, l_old);
+    new_iter = iter + 1;
+    if (compute_elbo) {
+      if (elbo_status != CV_OK) {
+        c_status = elbo_status;
+        done = 1;
+      } else {
+        if (have_prev && fabs(elbo - prev_elbo) < rel_tol * fabs(elbo)) done = 1;
+        new_prev = elbo;
+        new_have_prev = 1;
+      }
+    } else if (fmax(dk, fmax(dr, dl)) < param_tol) {
+      done = 1;
+    }
+    if (new_iter >= max_iter) done = 1;
+  }
+  if (status != CV_OK) {
+    c_status = status;
+    done = 1;
+  }
+
+  // ---- stores
+  s.status = status;
+  s.d = D;
+  s.V = (int64_t)h.V;
+  s.n_iter = mode == MODE_SWEEP ? n_iter_old + 1 : 0;
+  s.a_rho = a;
+  s.b_rho = b;
+  s.e_rho = e_rho;
+  s.ln_det_lam0l_inv = ld;
+  s.resid = st[NS - 2];
+  s.elbo = elbo;
+  s.elbo_status = elbo_status;
+  s.gen_lnA = gen.lnA;
+  s.gen_e_rho = gen.e_rho;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    s.k0k[i] = k_new[i];
+    s.e_lamk[i] = elamk[i];
     s.gen_c[i] = gen.c[i];
   }
 #pragma unroll
   for (int i = 0; i < D * D; ++i) {
+    s.lam0l_inv[i] = L[i];
+    s.e_lam[i] = h.nu * S[i];
     s.gen_A[i] = gen.A[i];
     s.gen_Ainv[i] = gen.Ainv[i];
   }
-  s.gen_lnA = gen.lnA;
-  s.gen_e_rho = gen.e_rho;
-  s.resid = stats[NS - 2];
-  s.elbo = qnan();
-  s.elbo_status = CV_OK;
-  if (status == CV_OK && (c.compute_elbo || c.mode == MODE_INIT)) {
-    int es;
-    s.elbo = elbo_t<D>(h, a, b, k_new, S, ld, gen, stats, &es);
-    s.elbo_status = es;
+  if (sweep_ok && iter < tr_cap) {
+    tr_dk[iter] = dk;
+    tr_drho[iter] = dr;
+    tr_dlam[iter] = dl;
+    tr_elbo[iter] = compute_elbo ? elbo : qnan();
   }
-  if (c.mode == MODE_SWEEP) {
-    s.n_iter = s.n_iter + 1;
-    if (status == CV_OK) {
-      // fit bookkeeping (vb.py:332-347)
-      const double dk = rel_delta_t<D>(k_new, k_old);
-      const double dr = rel_delta_t<1>(&e_rho, &e_rho_old);
-      const double dl = rel_delta_t<D * D>(L, l_old);
-      const int it = c.iter;
-      if (it < c.tr_cap) {
-        c.tr_dk[it] = dk;
-        c.tr_drho[it] = dr;
-        c.tr_dlam[it] = dl;
-        c.tr_elbo[it] = c.compute_elbo ? s.elbo : qnan();
-      }
-      c.iter = it + 1;
-      if (c.compute_elbo) {
-        if (s.elbo_status != CV_OK) {
-          c.status = s.elbo_status;
-          c.done = 1;
-        } else {
-          if (c.have_prev && fabs(s.elbo - c.prev_elbo) < c.rel_tol * fabs(s.elbo)) c.done = 1;
-          c.prev_elbo = s.elbo;
-          c.have_prev = 1;
-        }
-      } else if (fmax(dk, fmax(dr, dl)) < c.param_tol) {
-        c.done = 1;
-      }
-      if (c.iter >= c.max_iter) c.done = 1;
-    }
-  } else {
-    s.n_iter = 0;
-  }
-  if (status != CV_OK) {
-    c.status = status;
-    c.done = 1;
-  }
+  c.iter = new_iter;
+  c.have_prev = new_have_prev;
+  c.prev_elbo = new_prev;
+  if (c_status != CV_OK) c.status = c_status;
+  if (done) c.done = 1;
   c.mode = MODE_SWEEP;
-  if (status == CV_OK) derive_pass_t<D>(h, c);
+  if (status == CV_OK) {
+    // generator of the next pass (vb.py:136-144)
+    const double rnu = 1.0 / h.nu;
+#pragma unroll
+    for (int i = 0; i < D; ++i) c.pass.c[i] = k_new[i];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) {
+      c.pass.A[i] = h.nu * S[i];
+      c.pass.Ainv[i] = L[i] * rnu;
+    }
+    c.pass.lnA = D * h.ln_nu - ld;
+    const double nb = h.b0 + 0.5 * st[NS - 2];
+    c.pend_a = h.a_fit;
+    c.pend_b = nb;
+    c.pass.e_rho = h.a_fit / nb;
+  }
 }
 
 }  // namespace cavi

@@ -237,8 +237,8 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 
 template <int D, typename T>
 struct Geometry {
-  // consumer warps: 16 where the per-gene state fits ~100 registers, 8 for large d
-  static constexpr int kCons = D <= 7 ? 512 : 256;
+  // 8 consumer warps (16 measured slower: more per-tile sync, tail spills under the 120-register cap)
+  static constexpr int kCons = 256;
   static constexpr int kCWarps = kCons / 32;
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
