@@ -56,7 +56,7 @@ PassKernel pass_for(int d, int storage) {
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
     default:
-      return PassKernel{nullptr, 0, 0};
+      return PassKernel{nullptr, 0, 0, nullptr};
   }
 }
 
@@ -85,7 +85,8 @@ struct cv_dataset {
   double* trace = nullptr;
   int trace_cap = 0;
   int grid = 0;
-  PassKernel pass{nullptr, 0, 0};
+  PassKernel pass{nullptr, 0, 0, nullptr};
+  double* tot = nullptr;  // [ns] shard totals written by the pass, read by the tail kernel
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t graph = nullptr;
   int graph_unroll = 0;
@@ -141,6 +142,7 @@ int plan_and_alloc(cv_dataset* ds) {
   CK(cudaMalloc(&ds->ticket, sizeof(unsigned long long)));
   CK(cudaMemsetAsync(ds->ticket, 0, sizeof(unsigned long long), ds->stream));
   CK(cudaMalloc(&ds->opartials, sizeof(double) * ns * kOctants));
+  CK(cudaMalloc(&ds->tot, sizeof(double) * kMaxStats * kOctants));
   ds->n_live_octants = 0;
   for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
     const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
@@ -192,11 +194,23 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   return a;
 }
 
-int launch_pass(cv_dataset* ds) {
+int launch_pass_only(cv_dataset* ds) {
   if (ds->n_chunks == 0) return fail(CV_ERR_ARG, "empty shard");
-  ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, nullptr));
+  ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, ds->tot));
   CK(cudaGetLastError());
   return CV_OK;
+}
+
+int launch_tail_only(cv_dataset* ds) {
+  ds->pass.tail<<<1, 32, 0, ds->stream>>>(ds->hyp, ds->ctl, ds->tot, 1);
+  CK(cudaGetLastError());
+  return CV_OK;
+}
+
+// one sweep on a single GPU: the fused pass, then the one-warp tail
+int launch_pass(cv_dataset* ds) {
+  int rc = launch_pass_only(ds);
+  return rc ? rc : launch_tail_only(ds);
 }
 
 int check_hyper(cv_dataset* ds, const cv_hyper* hp) {
@@ -289,8 +303,10 @@ int ensure_graph(cv_dataset* ds, int unroll) {
   ds->graph = nullptr;
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(ds->stream, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < unroll; ++i)
-    ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, nullptr));
+  for (int i = 0; i < unroll; ++i) {
+    ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, ds->tot));
+    ds->pass.tail<<<1, 32, 0, ds->stream>>>(ds->hyp, ds->ctl, ds->tot, 1);
+  }
   cudaError_t e = cudaStreamEndCapture(ds->stream, &g);
   if (e != cudaSuccess) return fail(CV_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
   CK(cudaGraphInstantiate(&ds->graph, g, 0));
@@ -350,7 +366,7 @@ void cv_dataset_destroy(cv_dataset* ds) {
   if (ds->stream) cudaStreamSynchronize(ds->stream);
   if (ds->graph) cudaGraphExecDestroy(ds->graph);
   void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters, ds->ticket,
-                  ds->opartials,
+                  ds->opartials, ds->tot,
                   ds->flags, ds->ctl, ds->hyp, ds->trace};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -682,8 +698,9 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   CK(cudaEventRecord(ds->ev[0], ds->stream));
   for (int i = 0; i < sweeps; ++i) {
     CK(cudaEventRecord(evs[2 * i], ds->stream));
-    if ((rc = launch_pass(ds))) return rc;
-    CK(cudaEventRecord(evs[2 * i + 1], ds->stream));
+    if ((rc = launch_pass_only(ds))) return rc;
+    CK(cudaEventRecord(evs[2 * i + 1], ds->stream));  // brackets the fused pass kernel alone
+    if ((rc = launch_tail_only(ds))) return rc;
   }
   CK(cudaEventRecord(ds->ev[1], ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
@@ -714,7 +731,7 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   }
   *ms_kernel = k;
   for (auto& e : evs) cudaEventDestroy(e);
-  if (launches) *launches = sweeps;
+  if (launches) *launches = 2 * sweeps;  // fused pass + tail kernel per sweep
   if ((rc = ctl_get(ds))) return rc;
   if (ds->h_ctl->status != CV_OK) return state_status(ds->h_ctl->cur);
   return CV_OK;

@@ -445,7 +445,7 @@ static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
 // a single thread runs it at the end of every sweep, so its dependent global round trips
 // (not its flops) are what the sweep pays for.
 template <int D>
-__device__ __noinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
+__device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
   constexpr int NS = n_stats(D);
   // ---- loads (independent, issued back to back)
   HypT<D> h;

@@ -49,7 +49,7 @@ struct PassArgs {
   int n_live_octants;      // octants of this shard holding at least one group
   Ctl* ctl;
   const Hyp* hyp;
-  double* rank_out;        // multi-GPU: [ns] subtree partial of this shard; null -> run the tail
+  double* rank_out;        // [ns] totals of this shard (its octant subtree), read by the tail kernel
   unsigned long long* cta_trace;  // optional [grid][8] globaltimer stamps (diagnostics)
 };
 
@@ -59,6 +59,7 @@ struct PassKernel {
   PassFn fn;
   int threads;
   int smem;  // dynamic shared memory bytes
+  void (*tail)(const Hyp*, Ctl*, const double*, int);
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -183,7 +184,7 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
 
 // chunk partial -> group -> octant -> total (-> tail), by whichever warp completes each level
 template <int D, int NS = n_stats(D)>
-__device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, double* s_tot,
+__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, double* s_tot,
                                           int lane) {
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) a.partials[chunk * NS + st] = chunk_sum[st];
@@ -220,17 +221,32 @@ __device__ __noinline__ void finish_chunk(const PassArgs& a, int64_t chunk, cons
     }
     for (int w = 1; w < a.oct_hi - a.oct_lo; w *= 2)
       for (int q = a.oct_lo; q + w < a.oct_hi; q += 2 * w) v[q] = v[q] + v[q + w];
-    s_tot[st] = v[a.oct_lo];
-    if (a.rank_out) a.rank_out[st] = v[a.oct_lo];
+    a.rank_out[st] = v[a.oct_lo];
   }
-  __syncwarp();
-  if (a.rank_out) {
-    if (lane == 0) __threadfence();
-  } else if (lane == 0) {
-    tail_t<D>(*a.hyp, *a.ctl, s_tot);
-  }
+  (void)s_tot;
   if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
 }
+
+// The sweep tail as its own one-warp kernel (full register file: the tail is a long
+// dependent scalar chain and must not spill): pairwise tree over the `world` shard
+// totals (1 on a single GPU; the NCCL-gathered rank partials otherwise), then tail_t.
+template <int D>
+__global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, Ctl* c, const double* parts, int world) {
+  constexpr int NS = n_stats(D);
+  __shared__ double tot[NS];
+  if (*(volatile const int*)&c->done) return;
+  for (int st = threadIdx.x; st < NS; st += 32) {
+    double v[kOctants];
+    for (int r = 0; r < world; ++r) v[r] = __ldcg(parts + r * NS + st);
+    for (int w = 1; w < world; w *= 2)
+      for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
+    tot[st] = v[0];
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) tail_t<D>(*h, *c, tot);
+}
+
+typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
 
 // ---------------------------------------------------------------- pipeline geometry
 constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles < kSlots chunks)

@@ -17,6 +17,7 @@ static cavi::PassKernel make_kernel() {
   k.fn = cavi::pass_kernel<CAVI_D, T>;
   k.threads = G::kCtaThreads;
   k.smem = G::kSmem;
+  k.tail = cavi::tail_kernel<CAVI_D>;
   cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   return k;
 }
