@@ -1,8 +1,10 @@
 # Builds the in-tree CUDA library (sm_100a) that the Python drop-in loads.
 #   make -j16            -> paper_2401_10068_b200/libcavi.so
 NVCC ?= /usr/local/cuda/bin/nvcc
+PY_SITE ?= $(shell python -c 'import sysconfig; print(sysconfig.get_paths()["purelib"])')
+NCCL_HOME ?= $(PY_SITE)/nvidia/nccl
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 $(ARCH) -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+NVFLAGS := -O3 $(ARCH) -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -I$(NCCL_HOME)/include
 PKG := paper_2401_10068_b200
 CSRC := $(PKG)/csrc
 BUILD := build/obj
@@ -23,7 +25,7 @@ $(BUILD)/cavi.o: $(CSRC)/cavi.cu $(HDR) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
 $(LIB): $(BUILD)/cavi.o $(PASS_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib
 
 ptxas: | $(BUILD)
 	$(NVCC) $(NVFLAGS) -DCAVI_D=3 -Xptxas -v -c -o $(BUILD)/ptxas_d3.o $(CSRC)/pass_inst.cu

@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--profile", action="store_true", help="under ncu: no clock soak, no e2e/cpu legs")
+    p.add_argument("--force-dist", action="store_true", help="use the sharded NCCL path even at N=1")
     p.add_argument("--converge", action="store_true", help="also time vb_fit to ELBO convergence")
     return p.parse_args()
 
@@ -193,7 +194,7 @@ def run_ours(args):
     from paper_2401_10068_b200 import _lib, model, vb
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world != 1 or args.gpus != 1:
+    if world != 1 or args.gpus != 1 or args.force_dist:
         from paper_2401_10068_b200 import dist  # noqa: PLC0415
 
         return dist.bench_main(args, METRIC, UNIT)

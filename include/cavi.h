@@ -90,6 +90,7 @@ typedef struct cv_state {
 } cv_state;
 
 typedef struct cv_dataset cv_dataset;
+typedef struct cv_comm cv_comm;
 
 /* ---- library ---------------------------------------------------------- */
 int32_t cv_abi_version(void);
@@ -114,6 +115,23 @@ int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, do
 int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo, int64_t* V_total,
                         int32_t* storage, int64_t* device_bytes);
 void cv_dataset_destroy(cv_dataset* ds);
+
+/* ---- multi-GPU (one process per GPU; NCCL over NVLink) ---------------- */
+/* The dataset is split into 8 octants of whole 64x4096-gene groups; rank r of a
+ * world of 1/2/4/8 owns octants [8r/world, 8(r+1)/world) (the gene range the
+ * Python planner `dist.shard_ranges` computes).  Per sweep the ranks exchange
+ * one n_stats(d)-double partial (ncclAllGather) and all run the identical tail,
+ * so states, traces and stop decisions agree bit-for-bit on every rank, and
+ * with the single-GPU result for any world size. */
+int32_t cv_nccl_unique_id(uint8_t* out /* 128 bytes */);
+int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t device, cv_comm** out);
+void cv_comm_destroy(cv_comm* c);
+int32_t cv_dataset_set_comm(cv_dataset* ds, cv_comm* comm);
+/* Mark a shard as rank `rank` of `world` without a communicator (single-GPU
+ * emulation of the multi-GPU reduction for tests) and return the shard's
+ * octant-subtree statistics of the sweep that would follow state `st`. */
+int32_t cv_dataset_set_shard(cv_dataset* ds, int32_t rank, int32_t world);
+int32_t cv_shard_stats(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* out);
 
 /* ---- the CAVI path --------------------------------------------------- */
 int32_t cv_init(cv_dataset* ds, const cv_hyper* hp, cv_state* out);

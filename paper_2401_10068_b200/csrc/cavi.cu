@@ -2,6 +2,7 @@
 // as CUDA graphs of fused-pass kernels (no host sync per sweep), and the C ABI
 // declared in include/cavi.h.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -62,8 +63,15 @@ PassKernel pass_for(int d, int storage) {
 
 }  // namespace
 
+struct cv_comm {
+  ncclComm_t nccl = nullptr;
+  int rank = 0, world = 1, device = 0;
+};
+
 struct cv_dataset {
   int device = 0;
+  cv_comm* comm = nullptr;  // sharded datasets: one rank of a world of GPUs
+  double* gathered = nullptr;  // [world][ns] rank partials (allgather target)
   cudaStream_t stream = nullptr;
   int d = 0, storage = 0;
   int64_t V = 0, Vp = 0, gene_lo = 0, V_total = 0;
@@ -109,7 +117,8 @@ int plan_and_alloc(cv_dataset* ds) {
   ds->n_groups_total = (tot_chunks + kGroupChunks - 1) / kGroupChunks;
   ds->groups_per_octant = (ds->n_groups_total + kOctants - 1) / kOctants;
   const int64_t group_genes = (int64_t)kGroupChunks * kChunk;
-  if (ds->gene_lo % group_genes != 0) return fail(CV_ERR_ARG, "shard gene_lo %lld not group-aligned", (long long)ds->gene_lo);
+  if (ds->V > 0 && ds->gene_lo % group_genes != 0)
+    return fail(CV_ERR_ARG, "shard gene_lo %lld not group-aligned", (long long)ds->gene_lo);
   ds->group_lo = ds->gene_lo / group_genes;
   // octants this shard covers (must be whole octants unless the shard is the whole dataset)
   const int64_t oct_genes = ds->groups_per_octant * group_genes;
@@ -117,7 +126,7 @@ int plan_and_alloc(cv_dataset* ds) {
     ds->oct_lo = 0;
     ds->oct_hi = kOctants;
   } else {
-    if (ds->gene_lo % oct_genes != 0) return fail(CV_ERR_ARG, "shard not octant-aligned");
+    if (ds->V > 0 && ds->gene_lo % oct_genes != 0) return fail(CV_ERR_ARG, "shard not octant-aligned");
     ds->oct_lo = (int)(ds->gene_lo / oct_genes);
     int64_t hi = ds->gene_lo + ds->V;
     int oh = (int)((hi + oct_genes - 1) / oct_genes);
@@ -194,15 +203,35 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   return a;
 }
 
+double* rank_slot(cv_dataset* ds) {
+  return ds->comm ? ds->gathered + (size_t)ds->comm->rank * n_stats(ds->d) : ds->tot;
+}
+
 int launch_pass_only(cv_dataset* ds) {
-  if (ds->n_chunks == 0) return fail(CV_ERR_ARG, "empty shard");
-  ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, ds->tot));
+  if (ds->n_chunks == 0) {  // a rank that holds no genes contributes exact zeros
+    CK(cudaMemsetAsync(rank_slot(ds), 0, sizeof(double) * n_stats(ds->d), ds->stream));
+    return CV_OK;
+  }
+  ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, rank_slot(ds)));
   CK(cudaGetLastError());
   return CV_OK;
 }
 
+// multi-GPU exchange: every rank receives every rank's octant-subtree partial (88 B at d=3)
+int launch_exchange(cv_dataset* ds) {
+  if (!ds->comm) return CV_OK;
+  const int ns = n_stats(ds->d);
+  ncclResult_t r = ncclAllGather(ds->gathered + (size_t)ds->comm->rank * ns, ds->gathered, ns, ncclDouble,
+                                 ds->comm->nccl, ds->stream);
+  if (r != ncclSuccess) return fail(CV_ERR_CUDA, "ncclAllGather: %s", ncclGetErrorString(r));
+  return CV_OK;
+}
+
 int launch_tail_only(cv_dataset* ds) {
-  ds->pass.tail<<<1, 32, 0, ds->stream>>>(ds->hyp, ds->ctl, ds->tot, 1);
+  int rc = launch_exchange(ds);
+  if (rc) return rc;
+  const int world = ds->comm ? ds->comm->world : 1;
+  ds->pass.tail<<<1, 32, 0, ds->stream>>>(ds->hyp, ds->ctl, ds->comm ? ds->gathered : ds->tot, world);
   CK(cudaGetLastError());
   return CV_OK;
 }
@@ -303,11 +332,10 @@ int ensure_graph(cv_dataset* ds, int unroll) {
   ds->graph = nullptr;
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(ds->stream, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < unroll; ++i) {
-    ds->pass.fn<<<ds->grid, ds->pass.threads, ds->pass.smem, ds->stream>>>(pass_args(ds, ds->tot));
-    ds->pass.tail<<<1, 32, 0, ds->stream>>>(ds->hyp, ds->ctl, ds->tot, 1);
-  }
+  int rc = CV_OK;
+  for (int i = 0; i < unroll && rc == CV_OK; ++i) rc = launch_pass(ds);
   cudaError_t e = cudaStreamEndCapture(ds->stream, &g);
+  if (rc) return rc;
   if (e != cudaSuccess) return fail(CV_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
   CK(cudaGraphInstantiate(&ds->graph, g, 0));
   CK(cudaGraphDestroy(g));
@@ -328,9 +356,11 @@ int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, co
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * V * ds->d, cudaMemcpyHostToDevice, ds->stream));
   const int tb = 256;
   const int64_t blocks = (ds->Vp + tb - 1) / tb;
-  upload_kernel<T><<<(unsigned)blocks, tb, 0, ds->stream>>>(dr, dmu, dD, ds->V, ds->Vp, ds->d, (T*)ds->x, (T*)ds->D,
-                                                          ds->flags);
-  CK(cudaGetLastError());
+  if (blocks > 0) {
+    upload_kernel<T><<<(unsigned)blocks, tb, 0, ds->stream>>>(dr, dmu, dD, ds->V, ds->Vp, ds->d, (T*)ds->x,
+                                                            (T*)ds->D, ds->flags);
+    CK(cudaGetLastError());
+  }
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, ds->flags, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
@@ -346,6 +376,99 @@ int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, co
 extern "C" {
 
 int32_t cv_abi_version(void) { return 1; }
+
+int32_t cv_nccl_unique_id(uint8_t* out) {
+  if (!out) return fail(CV_ERR_ARG, "null pointer");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(CV_ERR_CUDA, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return CV_OK;
+}
+
+int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t device, cv_comm** out) {
+  if (!id || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (world != 1 && world != 2 && world != 4 && world != 8) return fail(CV_ERR_ARG, "world size must be 1, 2, 4 or 8");
+  if (rank < 0 || rank >= world) return fail(CV_ERR_ARG, "bad rank %d of %d", rank, world);
+  CK(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  cv_comm* c = new cv_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(CV_ERR_CUDA, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return CV_OK;
+}
+
+void cv_comm_destroy(cv_comm* c) {
+  if (!c) return;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+}
+
+int32_t cv_dataset_set_shard(cv_dataset* ds, int32_t rank, int32_t world) {
+  if (!ds) return fail(CV_ERR_ARG, "null pointer");
+  if ((world != 1 && world != 2 && world != 4 && world != 8) || rank < 0 || rank >= world)
+    return fail(CV_ERR_ARG, "bad rank %d of world %d", rank, world);
+  // the shard must be exactly this rank's octant span of the dataset plan
+  const int per = kOctants / world;
+  const int64_t oct_genes = ds->groups_per_octant * (int64_t)kGroupChunks * kChunk;
+  const int64_t want_lo = std::min<int64_t>((int64_t)rank * per * oct_genes, ds->V_total);
+  const int64_t want_hi = std::min<int64_t>((int64_t)(rank + 1) * per * oct_genes, ds->V_total);
+  if (ds->gene_lo != want_lo && ds->V > 0) return fail(CV_ERR_ARG, "shard does not start at rank %d's octant span", rank);
+  if (ds->gene_lo + ds->V != want_hi && ds->V > 0) return fail(CV_ERR_ARG, "shard is not rank %d's octant span", rank);
+  ds->oct_lo = rank * per;
+  ds->oct_hi = ds->oct_lo + per;
+  ds->n_live_octants = 0;
+  for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
+    const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
+    const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
+                                         ds->group_lo + ds->n_groups);
+    if (h1 > h0) ++ds->n_live_octants;
+  }
+  if (ds->graph) {
+    CK(cudaGraphExecDestroy(ds->graph));
+    ds->graph = nullptr;
+  }
+  return CV_OK;
+}
+
+int32_t cv_dataset_set_comm(cv_dataset* ds, cv_comm* comm) {
+  if (!ds || !comm) return fail(CV_ERR_ARG, "null pointer");
+  if (comm->device != ds->device) return fail(CV_ERR_ARG, "communicator and dataset on different devices");
+  int rc = cv_dataset_set_shard(ds, comm->rank, comm->world);
+  if (rc) return rc;
+  CK(cudaSetDevice(ds->device));
+  if (ds->gathered) CK(cudaFree(ds->gathered));
+  CK(cudaMalloc(&ds->gathered, sizeof(double) * n_stats(ds->d) * comm->world));
+  CK(cudaMemsetAsync(ds->gathered, 0, sizeof(double) * n_stats(ds->d) * comm->world, ds->stream));
+  ds->comm = comm;
+  return CV_OK;
+}
+
+int32_t cv_shard_stats(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* out) {
+  if (!ds || !st || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (ds->comm) return fail(CV_ERR_ARG, "cv_shard_stats is for shards without a communicator");
+  int rc = upload_hyper(ds, hp);
+  if (rc) return rc;
+  Ctl c;
+  reset_ctl(c);
+  c.cur = *st;
+  c.mode = MODE_SWEEP;
+  if ((rc = ctl_put(ds, c))) return rc;
+  derive_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
+  CK(cudaGetLastError());
+  if ((rc = launch_pass_only(ds))) return rc;
+  CK(cudaMemcpyAsync(out, ds->tot, sizeof(double) * n_stats(ds->d), cudaMemcpyDeviceToHost, ds->stream));
+  CK(cudaStreamSynchronize(ds->stream));
+  return CV_OK;
+}
 
 const char* cv_last_error(void) { return g_err.c_str(); }
 
@@ -366,7 +489,7 @@ void cv_dataset_destroy(cv_dataset* ds) {
   if (ds->stream) cudaStreamSynchronize(ds->stream);
   if (ds->graph) cudaGraphExecDestroy(ds->graph);
   void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters, ds->ticket,
-                  ds->opartials, ds->tot,
+                  ds->opartials, ds->tot, ds->gathered,
                   ds->flags, ds->ctl, ds->hyp, ds->trace};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -379,7 +502,8 @@ void cv_dataset_destroy(cv_dataset* ds) {
 
 static int new_dataset(int64_t V, int32_t d, int64_t gene_lo, int64_t V_total, int32_t storage, int32_t device,
                        cv_dataset** out) {
-  if (V < 1) return fail(CV_ERR_ARG, "empty dataset");
+  if (V < 0 || V_total < 1 || (V == 0 && V_total == 0)) return fail(CV_ERR_ARG, "empty dataset");
+  if (V == 0 && gene_lo == 0 && V_total == 0) return fail(CV_ERR_ARG, "empty dataset");
   if (d < 1 || d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
   if (storage != CV_STORE_F64 && storage != CV_STORE_F32) return fail(CV_ERR_ARG, "bad storage %d", storage);
   if (gene_lo < 0 || V_total < gene_lo + V) return fail(CV_ERR_ARG, "shard [%lld, %lld) outside %lld genes",
@@ -454,7 +578,8 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
   double* dL = nullptr;
   if (cudaMalloc(&dLam, sizeof(double) * 2 * kMaxD2) != cudaSuccess) return bail(fail(CV_ERR_CUDA, "cudaMalloc"));
   dL = dLam + kMaxD2;
-  if (cudaMalloc(&ds->r_raw, sizeof(double) * V) != cudaSuccess || cudaMalloc(&ds->mu_raw, sizeof(double) * V) != cudaSuccess) {
+  if (cudaMalloc(&ds->r_raw, sizeof(double) * std::max<int64_t>(V, 1)) != cudaSuccess ||
+      cudaMalloc(&ds->mu_raw, sizeof(double) * std::max<int64_t>(V, 1)) != cudaSuccess) {
     cudaFree(dLam);
     return bail(fail(CV_ERR_CUDA, "cudaMalloc raw"));
   }
@@ -475,9 +600,9 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
   }
   const int tb = 256;
   const unsigned blocks = (unsigned)((ds->Vp + tb - 1) / tb);
-  if (storage == CV_STORE_F32)
+  if (blocks > 0 && storage == CV_STORE_F32)
     gen_kernel<float><<<blocks, tb, 0, ds->stream>>>(a, dL);
-  else
+  else if (blocks > 0)
     gen_kernel<double><<<blocks, tb, 0, ds->stream>>>(a, dL);
   e = cudaStreamSynchronize(ds->stream);
   cudaFree(dLam);
@@ -528,7 +653,7 @@ int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo
 
 int32_t cv_init(cv_dataset* ds, const cv_hyper* hp, cv_state* out) {
   if (!ds || !out) return fail(CV_ERR_ARG, "null pointer");
-  if (ds->V != ds->V_total) return fail(CV_ERR_ARG, "cv_init on a shard: use the sharded driver");
+  if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_init on a shard needs cv_dataset_set_comm");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
   rc = run_init(ds, 1);
@@ -585,7 +710,7 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
                int32_t* n_iter) {
   if (!ds || !out || !n_iter) return fail(CV_ERR_ARG, "null pointer");
   if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
-  if (ds->V != ds->V_total) return fail(CV_ERR_ARG, "cv_fit on a shard: use the sharded driver");
+  if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_fit on a shard needs cv_dataset_set_comm");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
   if ((rc = ensure_trace(ds, max_iter))) return rc;

@@ -1,0 +1,69 @@
+"""Multi-GPU reduction on one GPU: shards of 1/2/4/8 ranks (emulated, no cross-kernel
+waiting) combine to the single-GPU statistics bit-exactly, and the NCCL path
+(a world-1 communicator inside the captured sweep graph) reproduces the
+single-GPU fit bit-exactly."""
+
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def tree(parts):
+    parts = list(parts)
+    while len(parts) > 1:
+        parts = [parts[i] + parts[i + 1] for i in range(0, len(parts), 2)]
+    return parts[0]
+
+
+@pytest.mark.parametrize("V,N", [(3_000_001, 4), (777_777, 3), (20_000, 6)])
+def test_shard_partials_combine_bit_exact(V, N):
+    from paper_2401_10068_b200 import _lib, dist, model, vb
+
+    K, lam = np.full(N - 1, 0.2), np.linalg.inv(0.01 * np.eye(N - 1))
+    hp = model.default_hyperparams(N)
+    full = model.generate(9, V, N, K, lam, 100.0)
+    st, _ = vb.vb_fit(full, hp, max_iter=4)
+    hs, keep = _lib.hyper_struct(hp)
+    ns = (N - 1) + (N - 1) * N // 2 + 2
+
+    def stats(dd, rank, world):
+        _lib.check(_lib.lib().cv_dataset_set_shard(dd.handle, rank, world))
+        out = np.empty(ns)
+        _lib.check(_lib.lib().cv_shard_stats(dd.handle, C.byref(hs), C.byref(st._cs), _lib.dptr(out)))
+        return out
+
+    whole = stats(full, 0, 1)
+    for world in (2, 4, 8):
+        parts = []
+        for rk, (lo, hi) in enumerate(dist.shard_ranges(V, world)):
+            dd = model.generate(9, hi - lo, N, K, lam, 100.0, gene_lo=lo, V_total=V)
+            parts.append(stats(dd, rk, world))
+        assert np.array_equal(tree(parts), whole), f"world {world}"
+
+
+def test_nccl_world1_fit_equals_single_gpu():
+    import torch.distributed as td
+
+    from paper_2401_10068_b200 import dist, model, vb
+
+    if not td.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        td.init_process_group("gloo", rank=0, world_size=1)
+    comm = dist.Comm.bootstrap(device=0, td=td)
+    V, N = 1_500_000, 4
+    K, lam = np.full(3, 0.2), np.linalg.inv(0.01 * np.eye(3))
+    hp = model.default_hyperparams(N)
+    ref_st, ref_tr = vb.vb_fit(model.generate(5, V, N, K, lam, 100.0), hp, max_iter=30)
+    shard = dist.shard_generate(5, V, N, K, lam, 100.0, comm)
+    st, tr = vb.vb_fit(shard, hp, max_iter=30)
+    assert np.array_equal(tr.elbo, ref_tr.elbo)
+    assert np.array_equal(st.lam0l_inv, ref_st.lam0l_inv) and st.b_rho == ref_st.b_rho
