@@ -146,6 +146,15 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
 int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int64_t lo, int64_t hi,
                        double* mu_beta, double* lam_beta, double* e_bbt);
 
+/* ---- many independent fits (BASELINE config 4) --------------------------- */
+/* vb_fit on each of n_fits datasets (genes [offsets[f], offsets[f+1]) of r, mu, D),
+ * all with hyperparameters hp, one warp per fit on `device`.  out: n_fits states;
+ * traces (optional): [n_fits][4][max_iter] = elbo, delta_k0k, delta_rho, delta_lam per
+ * sweep (NaN past each fit's n_iter = out[f].n_iter). */
+int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
+                       int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+                       double param_tol, int32_t device, cv_state* out, double* traces);
+
 /* ---- pinned host memory (for end-to-end uploads at DMA speed) --------- */
 int32_t cv_host_alloc(int64_t bytes, void** out);
 void cv_host_free(void* p);

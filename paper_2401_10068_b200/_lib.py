@@ -88,6 +88,8 @@ _SIGS = {
     "cv_dataset_set_comm": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "cv_dataset_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
+    "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
+                                   C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
     "cv_host_alloc": (C.c_int32, [C.c_int64, _P(C.c_void_p)]),
     "cv_host_free": (None, [C.c_void_p]),
     "cv_bench_sweeps": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), C.c_int32, C.c_int32, _D, _D,

@@ -57,7 +57,7 @@ PassKernel pass_for(int d, int storage) {
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
     default:
-      return PassKernel{nullptr, 0, 0, nullptr};
+      return PassKernel{nullptr, 0, 0, nullptr, nullptr};
   }
 }
 
@@ -93,7 +93,7 @@ struct cv_dataset {
   double* trace = nullptr;
   int trace_cap = 0;
   int grid = 0;
-  PassKernel pass{nullptr, 0, 0, nullptr};
+  PassKernel pass{nullptr, 0, 0, nullptr, nullptr};
   double* tot = nullptr;  // [ns] shard totals written by the pass, read by the tail kernel
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t graph = nullptr;
@@ -788,6 +788,79 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
   if (dm) CK(cudaFree(dm));
   if (dl) CK(cudaFree(dl));
   if (de) CK(cudaFree(de));
+  return CV_OK;
+}
+
+int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
+                       int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+                       double param_tol, int32_t device, cv_state* out, double* traces) {
+  if (!r || !mu || !D || !offsets || !hp || !out) return fail(CV_ERR_ARG, "null pointer");
+  if (n_fits < 1) return fail(CV_ERR_ARG, "no fits");
+  if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
+  if (d < 1 || d > kMaxD || hp->d != d) return fail(CV_ERR_ARG, "hyperparams dim %d != dataset dim %d", hp->d, d);
+  if (!(hp->a0 > 0 && hp->b0 > 0 && hp->q0 > 0 && hp->n0 >= 1)) return fail(CV_ERR_ARG, "hyperparameters must be positive");
+  if (offsets[0] != 0) return fail(CV_ERR_ARG, "offsets must start at 0");
+  for (int64_t f = 0; f < n_fits; ++f)
+    if (offsets[f + 1] <= offsets[f]) return fail(CV_ERR_ARG, "fit %lld is empty", (long long)f);
+  const int64_t G = offsets[n_fits];
+  for (int64_t i = 0; i < G * d; ++i)
+    if (!std::isfinite(D[i])) return fail(CV_ERR_NONFINITE, "non-finite values in A");
+  PassKernel pk = pass_for(d, CV_STORE_F64);
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double *dr, *dmu, *dD, *dtr;
+  int64_t* doff;
+  Hyp *base, *hyps;
+  Ctl* ctls;
+  CK(cudaMalloc(&dr, sizeof(double) * G));
+  CK(cudaMalloc(&dmu, sizeof(double) * G));
+  CK(cudaMalloc(&dD, sizeof(double) * G * d));
+  CK(cudaMalloc(&doff, sizeof(int64_t) * (n_fits + 1)));
+  CK(cudaMalloc(&base, sizeof(Hyp)));
+  CK(cudaMalloc(&hyps, sizeof(Hyp) * n_fits));
+  CK(cudaMalloc(&ctls, sizeof(Ctl) * n_fits));
+  CK(cudaMalloc(&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits));
+  CK(cudaMemcpyAsync(dr, r, sizeof(double) * G, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * G, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dD, D, sizeof(double) * G * d, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (n_fits + 1), cudaMemcpyHostToDevice, st));
+  Hyp h;
+  std::memset(&h, 0, sizeof h);
+  h.d = d;
+  h.n0 = hp->n0;
+  h.a0 = hp->a0;
+  h.b0 = hp->b0;
+  h.q0 = hp->q0;
+  for (int i = 0; i < d; ++i) h.K0[i] = hp->K0[i];
+  for (int i = 0; i < d * d; ++i) h.L0[i] = hp->Lambda0[i];
+  CK(cudaMemcpyAsync(base, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctls, 0, sizeof(Ctl) * n_fits, st));
+  CK(cudaMemsetAsync(dtr, 0xFF, sizeof(double) * 4 * (size_t)max_iter * n_fits, st));  // NaN past n_iter
+  const unsigned sb = (unsigned)((n_fits + 63) / 64);
+  batched_setup_kernel<<<sb, 64, 0, st>>>(base, hyps, ctls, doff, n_fits, max_iter, rel_tol, compute_elbo ? 1 : 0,
+                                          param_tol, dtr);
+  CK(cudaGetLastError());
+  BatchArgs a{dr, dmu, dD, doff, n_fits, hyps, ctls};
+  const unsigned nb = (unsigned)((n_fits + kBatchWarps - 1) / kBatchWarps);
+  pk.batched<<<nb, kBatchWarps * 32, 0, st>>>(a);
+  CK(cudaGetLastError());
+  // states are the first member of each control block: one strided copy
+  CK(cudaMemcpy2DAsync(out, sizeof(cv_state), ctls, sizeof(Ctl), sizeof(cv_state), n_fits, cudaMemcpyDeviceToHost,
+                       st));
+  if (traces)
+    CK(cudaMemcpyAsync(traces, dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, cudaMemcpyDeviceToHost, st));
+  std::vector<int> status(n_fits);
+  CK(cudaMemcpy2DAsync(status.data(), sizeof(int), &ctls[0].status, sizeof(Ctl), sizeof(int), n_fits,
+                       cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (void* p : {(void*)dr, (void*)dmu, (void*)dD, (void*)doff, (void*)base, (void*)hyps, (void*)ctls, (void*)dtr})
+    cudaFree(p);
+  cudaStreamDestroy(st);
+  for (int64_t f = 0; f < n_fits; ++f) {
+    if (status[f] == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "fit %lld: Q(Lambda) is improper; dataset too small", (long long)f);
+    if (status[f] != CV_OK) return fail(status[f], "fit %lld failed with status %d", (long long)f, status[f]);
+  }
   return CV_OK;
 }
 

@@ -2,7 +2,7 @@
 // hand-over, the multi-GPU tail).  Included by cavi.cu only.
 #pragma once
 
-#include "pass.cuh"
+#include "batched.cuh"
 
 namespace cavi {
 
@@ -42,6 +42,33 @@ __global__ void state_gen_kernel(Ctl* c, int d) {
     }
     c->pass.lnA = s.gen_lnA;
     c->pass.e_rho = s.gen_e_rho;
+  }
+}
+
+// Per-fit hyperparameter constants and control blocks of a batched fit.
+__global__ void batched_setup_kernel(const Hyp* base, Hyp* hyps, Ctl* ctls, const int64_t* offsets, int64_t n_fits,
+                                     int max_iter, double rel_tol, int compute_elbo, double param_tol,
+                                     double* traces) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_fits) return;
+  Hyp& h = hyps[f];
+  h = *base;
+  h.V = (double)(offsets[f + 1] - offsets[f]);
+  hyp_setup(h);
+  Ctl& c = ctls[f];
+  c.max_iter = max_iter;
+  c.rel_tol = rel_tol;
+  c.param_tol = param_tol;
+  c.compute_elbo = compute_elbo;
+  c.tr_cap = max_iter;
+  double* t = traces + (size_t)f * 4 * max_iter;
+  c.tr_elbo = t;
+  c.tr_dk = t + max_iter;
+  c.tr_drho = t + 2 * (size_t)max_iter;
+  c.tr_dlam = t + 3 * (size_t)max_iter;
+  if (h.setup_status != CV_OK) {
+    c.status = h.setup_status;
+    c.done = 1;
   }
 }
 

@@ -54,12 +54,14 @@ struct PassArgs {
 };
 
 typedef void (*PassFn)(PassArgs);
+struct BatchArgs;
 
 struct PassKernel {
   PassFn fn;
   int threads;
   int smem;  // dynamic shared memory bytes
   void (*tail)(const Hyp*, Ctl*, const double*, int);
+  void (*batched)(BatchArgs);
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -1,7 +1,7 @@
 // pass_inst.cu -- one explicit instantiation set of the fused pass per
 // dimension; the Makefile compiles this file once per CAVI_D in 1..15 so the
 // builds run in parallel.
-#include "pass.cuh"
+#include "batched.cuh"
 
 #ifndef CAVI_D
 #error "compile with -DCAVI_D=<1..15>"
@@ -18,6 +18,7 @@ static cavi::PassKernel make_kernel() {
   k.threads = G::kCtaThreads;
   k.smem = G::kSmem;
   k.tail = cavi::tail_kernel<CAVI_D>;
+  k.batched = cavi::batched_fit_kernel<CAVI_D>;
   cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   return k;
 }

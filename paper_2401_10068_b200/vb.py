@@ -31,7 +31,8 @@ import numpy as np
 
 from . import _lib, linalg, model
 
-__all__ = ["VbState", "VbTrace", "install", "vb_elbo", "vb_fit", "vb_init", "vb_posterior_sample", "vb_step"]
+__all__ = ["VbState", "VbTrace", "install", "vb_elbo", "vb_fit", "vb_fit_many", "vb_init", "vb_posterior_sample",
+           "vb_step"]
 
 # ---------------------------------------------------------------- dataset residency
 _resident: dict[int, tuple] = {}
@@ -130,15 +131,16 @@ class VbState:
 
     # --- per-gene fields, materialised on demand
     def _materialise(self):
-        if not self._lazy:
-            V, d = self._dds.V, self._dds.dim
+        if "mu_beta" not in self._lazy:
+            dds = self._dds if self._dds is not None else device_dataset(self._lazy["source"])
+            V, d = dds.V, dds.dim
             if d != self.dim:
                 raise ValueError("state does not belong to this dataset")
             mu = np.empty((V, d))
             lam = np.empty((V, d, d))
             ebb = np.empty((V, d, d))
             hs, keep = _lib.hyper_struct(self._hp)
-            _lib.check(_lib.lib().cv_materialize(self._dds.handle, C.byref(hs), C.byref(self._cs), 0, V,
+            _lib.check(_lib.lib().cv_materialize(dds.handle, C.byref(hs), C.byref(self._cs), 0, V,
                                                  _lib.dptr(mu), _lib.dptr(lam), _lib.dptr(ebb)))
             self._lazy.update(mu_beta=self._ro(mu), lam_beta=self._ro(lam), e_bbt=self._ro(ebb))
         return self._lazy
@@ -251,6 +253,50 @@ def vb_fit(ds, hp, max_iter: int = 300, rel_tol: float = 1e-8, plan: linalg.Exec
     trace = VbTrace(elbo=tr[0, :k].copy(), delta_k0k=tr[1, :k].copy(), delta_rho=tr[2, :k].copy(),
                     delta_lam=tr[3, :k].copy())
     return VbState(out, dds, hp), trace
+
+
+def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, compute_elbo: bool = True,
+                param_tol: float = 1e-10, device: int | None = None):
+    """vb_fit on many independent datasets at once (BASELINE config 4: tissue samples).
+
+    One warp per fit runs the whole CAVI loop in-kernel (csrc/batched.cuh).  Returns a
+    list of (VbState, VbTrace), each equal to what vb_fit(ds, hp, ...) returns for
+    that dataset (within 1e-9, same iteration count).  The datasets must share N.
+    """
+    datasets = list(datasets)
+    if not datasets:
+        raise ValueError("no datasets")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    Ds = [np.ascontiguousarray(np.atleast_2d(ds.D), dtype=np.float64) for ds in datasets]
+    d = Ds[0].shape[1]
+    if any(Dm.shape[1] != d for Dm in Ds):
+        raise ValueError("all datasets must have the same number of networks")
+    hd = int(np.atleast_1d(hp.K0).shape[0])
+    if hd != d:
+        raise ValueError(f"hyperparams dim {hd} != dataset dim {d}")
+    r = np.ascontiguousarray(np.concatenate([np.atleast_1d(ds.r) for ds in datasets]), dtype=np.float64)
+    mu = np.ascontiguousarray(np.concatenate([np.atleast_1d(ds.mu) for ds in datasets]), dtype=np.float64)
+    D = np.ascontiguousarray(np.concatenate(Ds, axis=0))
+    offsets = np.zeros(len(datasets) + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum([Dm.shape[0] for Dm in Ds])
+    n = len(datasets)
+    states = (_lib.CvState * n)()
+    tr = np.empty((n, 4, max_iter))
+    hs, keep = _lib.hyper_struct(hp)
+    _lib.check(_lib.lib().cv_batched_fit(
+        _lib.dptr(r), _lib.dptr(mu), _lib.dptr(D), offsets.ctypes.data_as(C.POINTER(C.c_int64)), n, d,
+        C.byref(hs), int(max_iter), float(rel_tol), int(bool(compute_elbo)), float(param_tol),
+        _lib.default_device() if device is None else device, states, _lib.dptr(tr)))
+    out = []
+    for f, ds in enumerate(datasets):
+        cs = states[f].copy()
+        k = int(cs.n_iter)
+        st = VbState(cs, None, hp)
+        st._lazy["source"] = ds
+        out.append((st, VbTrace(elbo=tr[f, 0, :k].copy(), delta_k0k=tr[f, 1, :k].copy(),
+                                delta_rho=tr[f, 2, :k].copy(), delta_lam=tr[f, 3, :k].copy())))
+    return out
 
 
 def vb_posterior_sample(rng, state: VbState, hp, V: int, n_samples: int):

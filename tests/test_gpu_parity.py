@@ -148,3 +148,38 @@ def test_run_to_run_bit_identical(eng):
     a, ta = vb.vb_fit(dd, hp, max_iter=10)
     b, tb = vb.vb_fit(dd, hp, max_iter=10)
     assert np.array_equal(ta.elbo, tb.elbo) and np.array_equal(a.lam0l_inv, b.lam0l_inv)
+
+
+def test_batched_fits_match_reference_goldens(eng):
+    """Config 4: many fibroblast-shaped fits in one launch == per-fit reference vb_fit."""
+    vb, model = eng
+    gs = [Golden(n) for n in names("fit_fibro56_")]
+    datasets = [host_ds(model, g) for g in gs]
+    hp = hyper(model, gs[0])
+    res = vb.vb_fit_many(datasets * 3, hp)  # repeated datasets: independent warps, identical answers
+    for i, (st, tr) in enumerate(res):
+        g = gs[i % len(gs)]
+        assert len(tr) == int(g["n_iter"])
+        np.testing.assert_allclose(tr.elbo, g["elbo"], rtol=RTOL, atol=0)
+        np.testing.assert_allclose(tr.delta_k0k, g["delta_k0k"], rtol=1e-6, atol=1e-12)
+        close(st.k0k, g["k0k"])
+        close(st.lam0l_inv, g["lam0l_inv"])
+        close(st.b_rho, g["b_rho"])
+        close(st.mu_beta[g["idx"]], g["mu_beta"])
+    first, again = res[0], res[len(gs)]
+    assert np.array_equal(first[1].elbo, again[1].elbo)
+
+
+def test_batched_fits_mixed_sizes_match_single_fits(eng):
+    vb, model = eng
+    datasets, hp = [], model.default_hyperparams(3)
+    for s, V in enumerate([56, 1, 5, 200, 33, 1000]):
+        r, mu, D, _, _ = philox.make_regime(V, 100 + s, 3)
+        datasets.append(model.Dataset(r=r, mu=mu, D=D, n_networks=3))
+    res = vb.vb_fit_many(datasets, hp, max_iter=150)
+    for ds, (st, tr) in zip(datasets, res):
+        s1, t1 = vb.vb_fit(ds, hp, max_iter=150)
+        assert len(tr) == len(t1)
+        np.testing.assert_allclose(tr.elbo, t1.elbo, rtol=RTOL, atol=0)
+        close(st.k0k, s1.k0k)
+        close(st.lam0l_inv, s1.lam0l_inv)
