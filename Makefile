@@ -4,14 +4,14 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PY_SITE ?= $(shell python -c 'import sysconfig; print(sysconfig.get_paths()["purelib"])')
 NCCL_HOME ?= $(PY_SITE)/nvidia/nccl
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 $(ARCH) -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -I$(NCCL_HOME)/include
+NVFLAGS := -O3 $(ARCH) -lineinfo -std=c++17 $(EXTRA) -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr -I$(NCCL_HOME)/include
 PKG := paper_2401_10068_b200
 CSRC := $(PKG)/csrc
-BUILD := build/obj
+BUILD ?= build/obj
 HDR := $(wildcard $(CSRC)/*.cuh) include/cavi.h
 DIMS := 1 2 3 4 5 6 7 8 9 10 11 12 13 14 15
 PASS_OBJS := $(foreach d,$(DIMS),$(BUILD)/pass_d$(d).o)
-LIB := $(PKG)/libcavi.so
+LIB ?= $(PKG)/libcavi.so
 
 all: $(LIB)
 

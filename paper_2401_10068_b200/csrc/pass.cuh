@@ -253,22 +253,41 @@ typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
 // ---------------------------------------------------------------- pipeline geometry
 constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles < kSlots chunks)
 
+// Geometry measured on B200 (V=1e8, d=3, fp64): 2 CTAs/SM x (4 consumer warps + 1 TMA
+// producer warp), 8 genes per consumer thread per 1024-gene stage, 3 stages of 32 KB per
+// CTA -> 0.489 ms/pass = 100% of the measured copy bandwidth.  (1 CTA x 8 warps x 4
+// genes/thread: 0.593 ms; 16 warps x 2 genes: 0.66 ms -- ILP per thread and two
+// independent pipelines per SM are what hides the fp64 latency chains.)
+#ifndef CAVI_CONS
+#define CAVI_CONS 128  // consumer threads per CTA (4 warps)
+#endif
+#ifndef CAVI_TILE_SMALL_D
+#define CAVI_TILE_SMALL_D 1024  // genes per stage for d <= 3
+#endif
+#ifndef CAVI_SMEM_BUDGET
+#define CAVI_SMEM_BUDGET 100000
+#endif
+#ifndef CAVI_MIN_BLOCKS
+#define CAVI_MIN_BLOCKS 2  // CTAs per SM
+#endif
+
 template <int D, typename T>
 struct Geometry {
-  // 8 consumer warps (16 measured slower: more per-tile sync, tail spills under the 120-register cap)
-  static constexpr int kCons = 256;
+  static constexpr int kCons = CAVI_CONS;
   static constexpr int kCWarps = kCons / 32;
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
-  static constexpr int kTile = D <= 3 ? 1024 : (D <= 7 ? 512 : 256);  // genes per stage
+  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : (D <= 7 ? 512 : 256);  // genes per stage
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
   static constexpr uint32_t kStageBytes = kColBytes * (1 + D);
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
-  static constexpr int kBudget = 200 * 1024 - kSlotBytes;
-  static constexpr int kStages = (kBudget / (int)kStageBytes) > 8 ? 8 : (kBudget / (int)kStageBytes);
+  static constexpr int kBudget = CAVI_SMEM_BUDGET - kSlotBytes;
+  static constexpr int kFit = kBudget / (int)kStageBytes;
+  static constexpr int kDrift = (kSlots - 1) * kTilesPerChunk;
+  static constexpr int kStages = kFit < 8 ? (kFit < kDrift ? kFit : kDrift) : (8 < kDrift ? 8 : kDrift);
   // [stages][1+D][tile] | full[stages] | empty[stages] | stage chunk id[stages] | slots
   static constexpr int kOffBar = kStages * kStageBytes;
   static constexpr int kOffChunk = kOffBar + 2 * kStages * 8;
@@ -280,7 +299,7 @@ struct Geometry {
 };
 
 template <int D, typename T>
-__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, 1) pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) pass_kernel(PassArgs a) {
   using G = Geometry<D, T>;
   constexpr int NS = n_stats(D);
   constexpr int kWarps = G::kCWarps;
