@@ -108,6 +108,23 @@ namespace {
 
 size_t elem(int storage) { return storage == CV_STORE_F32 ? sizeof(float) : sizeof(double); }
 
+// Stream-ordered pool allocations for everything whose lifetime is a dataset: repeated
+// uploads (the end-to-end path) then reuse HBM instead of paying cudaMalloc/cudaFree of
+// gigabyte buffers (the device pool keeps freed memory: release threshold = max).
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s, int device) {
+  static bool configured[64] = {false};
+  if (device >= 0 && device < 64 && !configured[device]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    configured[device] = true;
+  }
+  return cudaMallocAsync(p, std::max<size_t>(bytes, 16), s);
+}
+#define PALLOC(ptr, bytes) CK(pool_alloc((void**)&(ptr), (bytes), ds->stream, ds->device))
+
 int plan_and_alloc(cv_dataset* ds) {
   const int ns = n_stats(ds->d);
   ds->n_chunks = (ds->V + kChunk - 1) / kChunk;
@@ -142,16 +159,16 @@ int plan_and_alloc(cv_dataset* ds) {
   CK(cudaSetDevice(ds->device));
   CK(cudaStreamCreateWithFlags(&ds->stream, cudaStreamNonBlocking));
   const size_t nx = (size_t)std::max<int64_t>(ds->Vp, 2);
-  CK(cudaMalloc(&ds->x, nx * es));
-  CK(cudaMalloc(&ds->D, nx * es * ds->d));
-  CK(cudaMalloc(&ds->partials, sizeof(double) * ns * std::max<int64_t>(ds->n_chunks, 1)));
-  CK(cudaMalloc(&ds->gpartials, sizeof(double) * ns * std::max<int64_t>(ds->n_groups, 1)));
-  CK(cudaMalloc(&ds->counters, sizeof(unsigned int) * (ds->n_groups + kOctants + 1)));
+  PALLOC(ds->x, nx * es);
+  PALLOC(ds->D, nx * es * ds->d);
+  PALLOC(ds->partials, sizeof(double) * ns * std::max<int64_t>(ds->n_chunks, 1));
+  PALLOC(ds->gpartials, sizeof(double) * ns * std::max<int64_t>(ds->n_groups, 1));
+  PALLOC(ds->counters, sizeof(unsigned int) * (ds->n_groups + kOctants + 1));
   CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + kOctants + 1), ds->stream));
-  CK(cudaMalloc(&ds->ticket, sizeof(unsigned long long)));
+  PALLOC(ds->ticket, sizeof(unsigned long long));
   CK(cudaMemsetAsync(ds->ticket, 0, sizeof(unsigned long long), ds->stream));
-  CK(cudaMalloc(&ds->opartials, sizeof(double) * ns * kOctants));
-  CK(cudaMalloc(&ds->tot, sizeof(double) * kMaxStats * kOctants));
+  PALLOC(ds->opartials, sizeof(double) * ns * kOctants);
+  PALLOC(ds->tot, sizeof(double) * kMaxStats * kOctants);
   ds->n_live_octants = 0;
   for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
     const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
@@ -159,10 +176,10 @@ int plan_and_alloc(cv_dataset* ds) {
                                          ds->group_lo + ds->n_groups);
     if (h1 > h0) ++ds->n_live_octants;
   }
-  CK(cudaMalloc(&ds->flags, sizeof(int) * 4));
+  PALLOC(ds->flags, sizeof(int) * 4);
   CK(cudaMemsetAsync(ds->flags, 0, sizeof(int) * 4, ds->stream));
-  CK(cudaMalloc(&ds->ctl, sizeof(Ctl)));
-  CK(cudaMalloc(&ds->hyp, sizeof(Hyp)));
+  PALLOC(ds->ctl, sizeof(Ctl));
+  PALLOC(ds->hyp, sizeof(Hyp));
   CK(cudaMallocHost(&ds->h_ctl, sizeof(Ctl)));
   for (auto& e : ds->ev) CK(cudaEventCreate(&e));
   ds->device_bytes = nx * es * (1 + ds->d);
@@ -348,9 +365,9 @@ int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, co
   // stage the host arrays in HBM, then transform into the SoA stream
   double *dr = nullptr, *dmu = nullptr, *dD = nullptr;
   const size_t V = (size_t)ds->V;
-  CK(cudaMalloc(&dr, sizeof(double) * std::max<size_t>(V, 1)));
-  CK(cudaMalloc(&dmu, sizeof(double) * std::max<size_t>(V, 1)));
-  CK(cudaMalloc(&dD, sizeof(double) * std::max<size_t>(V * ds->d, 1)));
+  PALLOC(dr, sizeof(double) * std::max<size_t>(V, 1));
+  PALLOC(dmu, sizeof(double) * std::max<size_t>(V, 1));
+  PALLOC(dD, sizeof(double) * std::max<size_t>(V * ds->d, 1));
   CK(cudaMemcpyAsync(dr, r, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
   CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * V * ds->d, cudaMemcpyHostToDevice, ds->stream));
@@ -367,7 +384,7 @@ int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, co
   ds->bad_input = bad;
   ds->r_raw = dr;
   ds->mu_raw = dmu;
-  CK(cudaFree(dD));
+  CK(cudaFreeAsync(dD, ds->stream));
   return CV_OK;
 }
 
@@ -489,9 +506,11 @@ void cv_dataset_destroy(cv_dataset* ds) {
   if (ds->stream) cudaStreamSynchronize(ds->stream);
   if (ds->graph) cudaGraphExecDestroy(ds->graph);
   void* bufs[] = {ds->x, ds->D, ds->r_raw, ds->mu_raw, ds->partials, ds->gpartials, ds->counters, ds->ticket,
-                  ds->opartials, ds->tot, ds->gathered,
-                  ds->flags, ds->ctl, ds->hyp, ds->trace};
+                  ds->opartials, ds->tot, ds->flags, ds->ctl, ds->hyp};
   for (void* b : bufs)
+    if (b) cudaFreeAsync(b, ds->stream);  // back to the device pool (stream-ordered)
+  void* plain[] = {ds->gathered, ds->trace};
+  for (void* b : plain)
     if (b) cudaFree(b);
   if (ds->h_ctl) cudaFreeHost(ds->h_ctl);
   for (auto e : ds->ev)
@@ -578,8 +597,8 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
   double* dL = nullptr;
   if (cudaMalloc(&dLam, sizeof(double) * 2 * kMaxD2) != cudaSuccess) return bail(fail(CV_ERR_CUDA, "cudaMalloc"));
   dL = dLam + kMaxD2;
-  if (cudaMalloc(&ds->r_raw, sizeof(double) * std::max<int64_t>(V, 1)) != cudaSuccess ||
-      cudaMalloc(&ds->mu_raw, sizeof(double) * std::max<int64_t>(V, 1)) != cudaSuccess) {
+  if (pool_alloc((void**)&ds->r_raw, sizeof(double) * std::max<int64_t>(V, 1), ds->stream, ds->device) != cudaSuccess ||
+      pool_alloc((void**)&ds->mu_raw, sizeof(double) * std::max<int64_t>(V, 1), ds->stream, ds->device) != cudaSuccess) {
     cudaFree(dLam);
     return bail(fail(CV_ERR_CUDA, "cudaMalloc raw"));
   }
