@@ -155,6 +155,16 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
                        int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
                        double param_tol, int32_t device, cv_state* out, double* traces);
 
+/* ---- posterior draws (vb_posterior_sample, vb.py:357-393) -------------- */
+/* n joint draws of (K, Lambda, rho) from the fitted Q of a state with globals
+ * (a_rho, b_rho, k0k, lam0l_inv), consuming the Philox stream (seed, stream_id)
+ * from block `block0` exactly as the reference RngStream does; *block_end is the
+ * stream position afterwards.  K_out (n,d), Lam_out (n,d,d), rho_out (n). */
+int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, int32_t d, int32_t n0, double q0,
+                            int64_t V, double a_rho, double b_rho, const double* k0k, const double* lam0l_inv,
+                            int64_t n, int32_t device, double* K_out, double* Lam_out, double* rho_out,
+                            uint64_t* block_end);
+
 /* ---- pinned host memory (for end-to-end uploads at DMA speed) --------- */
 int32_t cv_host_alloc(int64_t bytes, void** out);
 void cv_host_free(void* p);

@@ -295,3 +295,60 @@ __all__ = [
     "e_ln_det", "elbo", "fit", "init", "inv_retry", "pairwise", "rel_delta", "resid_sum",
     "spans", "step", "wishart_log_z",
 ]
+
+
+# ------------------------------------------------------------ posterior draws
+def _gamma_ge1_many(stream, a: float, n: int) -> np.ndarray:
+    """Cubed-normal rejection, vectorised rounds (reference samplers.py:220-237)."""
+    d = a - 1.0 / 3.0
+    c = 1.0 / np.sqrt(9.0 * d)
+    out = np.empty(n)
+    filled = 0
+    while filled < n:
+        todo = n - filled
+        u = stream.uniforms(todo)
+        x = stream.normals(todo)
+        v = (1.0 + c * x) ** 3
+        pos = v > 0.0
+        logv = np.full_like(v, -np.inf)
+        np.log(v, out=logv, where=pos)
+        ok = pos & (np.log(u) < 0.5 * x * x + d - d * v + d * logv)
+        k = int(np.count_nonzero(ok))
+        out[filled:filled + k] = d * v[ok]
+        filled += k
+    return out
+
+
+def gamma_many(stream, a: float, b: float, n: int) -> np.ndarray:
+    """sample_gamma(rng, GammaParams(a, b), size=n) (reference samplers.py:240-261)."""
+    if a >= 1.0:
+        raw = _gamma_ge1_many(stream, a, n)
+    else:
+        boost = _gamma_ge1_many(stream, a + 1.0, n)
+        u = stream.uniforms(n)
+        raw = boost * u ** (1.0 / a)
+    return raw / b
+
+
+def posterior_sample(stream, a_rho, b_rho, k0k, lam0l_inv, hp: Hyper, V: int, n: int):
+    """Joint (K, Lambda, rho) draws from the fitted Q (reference vb.py:357-393)."""
+    if n < 1:
+        raise ValueError("n_samples must be >= 1")
+    d = k0k.shape[0]
+    nu, qv = hp.n0 + V, hp.q0 + V
+    R = chol_lower(inv_small(lam0l_inv))
+    kd = np.empty((n, d))
+    ld = np.empty((n, d, d))
+    chunk = max(1, min(n, 4_000_000 // max(nu * d, 1)))
+    done = 0
+    while done < n:
+        m = min(chunk, n - done)
+        u = stream.normals(m * nu * d).reshape(m, nu, d)
+        S = u @ R.T
+        lam = np.einsum("mnd,mne->mde", S, S)
+        ld[done:done + m] = lam
+        Lk = chol_lower(inv_small(qv * lam))
+        uk = stream.normals(m * d).reshape(m, d)
+        kd[done:done + m] = k0k + np.einsum("mij,mj->mi", Lk, uk)
+        done += m
+    return {"K": kd, "Lambda": ld, "rho": np.asarray(gamma_many(stream, a_rho, b_rho, n))}

@@ -90,6 +90,9 @@ _SIGS = {
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
     "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
                                    C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
+    "cv_posterior_sample": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
+                                        C.c_int64, C.c_double, C.c_double, _D, _D, C.c_int64, C.c_int32, _D, _D, _D,
+                                        _P(C.c_uint64)]),
     "cv_host_alloc": (C.c_int32, [C.c_int64, _P(C.c_void_p)]),
     "cv_host_free": (None, [C.c_void_p]),
     "cv_bench_sweeps": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), C.c_int32, C.c_int32, _D, _D,

@@ -14,6 +14,9 @@
 
 #include "gen.cuh"
 #include "control.cuh"
+#include "posterior.cuh"
+
+#include <cub/cub.cuh>
 
 using namespace cavi;
 
@@ -57,7 +60,7 @@ PassKernel pass_for(int d, int storage) {
     CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
     default:
-      return PassKernel{nullptr, 0, 0, nullptr, nullptr};
+      return PassKernel{nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
   }
 }
 
@@ -93,7 +96,7 @@ struct cv_dataset {
   double* trace = nullptr;
   int trace_cap = 0;
   int grid = 0;
-  PassKernel pass{nullptr, 0, 0, nullptr, nullptr};
+  PassKernel pass{nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
   double* tot = nullptr;  // [ns] shard totals written by the pass, read by the tail kernel
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t graph = nullptr;
@@ -880,6 +883,112 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
     if (status[f] == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "fit %lld: Q(Lambda) is improper; dataset too small", (long long)f);
     if (status[f] != CV_OK) return fail(status[f], "fit %lld failed with status %d", (long long)f, status[f]);
   }
+  return CV_OK;
+}
+
+int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, int32_t d, int32_t n0, double q0,
+                            int64_t V, double a_rho, double b_rho, const double* k0k, const double* lam0l_inv,
+                            int64_t n, int32_t device, double* K_out, double* Lam_out, double* rho_out,
+                            uint64_t* block_end) {
+  if (!k0k || !lam0l_inv || !K_out || !Lam_out || !rho_out || !block_end) return fail(CV_ERR_ARG, "null pointer");
+  if (n < 1) return fail(CV_ERR_ARG, "n_samples must be >= 1");
+  if (d < 1 || d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported", d);
+  if (!(a_rho > 0 && b_rho > 0)) return fail(CV_ERR_ARG, "gamma parameters must be positive, got a=%g, b=%g", a_rho, b_rho);
+  PassKernel pk = pass_for(d, CV_STORE_F64);
+  CK(cudaSetDevice(device));
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int np = d * (d + 1) / 2;
+  const int64_t nu = (int64_t)n0 + V;
+  const double qv = q0 + (double)V;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 4000000 / std::max<int64_t>(nu * d, 1)));
+  const int64_t n_seg = (nu + kPostSegRows - 1) / kPostSegRows;
+  double *dLam, *dR, *dk0k, *lam_d, *k_d, *seg, *val, *raw, *rho_d;
+  char* flags;
+  int64_t* nsel;
+  int* prep;
+  CK(cudaMalloc(&dLam, sizeof(double) * 2 * kMaxD2));
+  dR = dLam + kMaxD2;
+  CK(cudaMalloc(&dk0k, sizeof(double) * kMaxD));
+  CK(cudaMalloc(&lam_d, sizeof(double) * n * d * d));
+  CK(cudaMalloc(&k_d, sizeof(double) * n * d));
+  const int64_t max_m = std::min<int64_t>(chunk, 65535);
+  CK(cudaMalloc(&seg, sizeof(double) * std::max<int64_t>(chunk, 1) * n_seg * np));
+  CK(cudaMalloc(&val, sizeof(double) * n));
+  CK(cudaMalloc(&raw, sizeof(double) * n));
+  CK(cudaMalloc(&rho_d, sizeof(double) * n));
+  CK(cudaMalloc(&flags, n));
+  CK(cudaMalloc(&nsel, sizeof(int64_t)));
+  CK(cudaMalloc(&prep, sizeof(int)));
+  CK(cudaMemcpyAsync(dLam, lam0l_inv, sizeof(double) * d * d, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dk0k, k0k, sizeof(double) * d, cudaMemcpyHostToDevice, st));
+  // R = chol(inv(lam0l_inv)) in the reference's operation order (vb.py:375-376)
+  gen_prep_kernel<<<1, 1, 0, st>>>(dLam, dR, d, prep);
+  uint64_t block = block0;
+  for (int64_t done = 0; done < n;) {
+    const int64_t m = std::min<int64_t>(chunk, n - done);
+    WishartArgs wa;
+    wa.seed = seed;
+    wa.stream_id = stream_id;
+    wa.d = d;
+    wa.nu = nu;
+    wa.n_draws = m;
+    wa.block0 = block;
+    wa.n_seg = n_seg;
+    wa.seg_out = seg;
+    for (int64_t k0 = 0; k0 < m; k0 += max_m) {
+      wa.k_base = k0;
+      const unsigned gy = (unsigned)std::min<int64_t>(max_m, m - k0);
+      pk.wishart_seg<<<dim3((unsigned)n_seg, gy), kPostThreads, 0, st>>>(wa);
+    }
+    CK(cudaGetLastError());
+    const uint64_t block_k = block + (uint64_t)((m * nu * d + 1) / 2);
+    wa.k_base = 0;
+    pk.wishart_fin<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(wa, dR, dk0k, qv, block_k, lam_d + done * d * d,
+                                                                k_d + done * d);
+    CK(cudaGetLastError());
+    block = block_k + (uint64_t)((m * d + 1) / 2);
+    done += m;
+  }
+  // rho ~ Gamma(a_rho, b_rho) by the reference's rejection rounds (samplers.py:220-261)
+  const bool boosted = !(a_rho >= 1.0);
+  const double ag = boosted ? a_rho + 1.0 : a_rho;
+  const double dd = ag - 1.0 / 3.0, cc = 1.0 / std::sqrt(9.0 * dd);
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, val, flags, raw, nsel, (int64_t)n, st));
+  CK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+  int64_t filled = 0;
+  while (filled < n) {
+    const int64_t todo = n - filled;
+    const uint64_t half = (uint64_t)((todo + 1) / 2);
+    gamma_round_kernel<<<(unsigned)((todo + 255) / 256), 256, 0, st>>>(seed, stream_id, block, block + half, todo, dd,
+                                                                       cc, val, flags);
+    CK(cudaGetLastError());
+    block += 2 * half;
+    CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, val, flags, raw + filled, nsel, todo, st));
+    int64_t k = 0;
+    CK(cudaMemcpyAsync(&k, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    filled += k;
+  }
+  const uint64_t bu = block;
+  if (boosted) block += (uint64_t)((n + 1) / 2);
+  gamma_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(raw, n, boosted ? 1 : 0, seed, stream_id, bu, a_rho,
+                                                                  b_rho, rho_d);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(K_out, k_d, sizeof(double) * n * d, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(Lam_out, lam_d, sizeof(double) * n * d * d, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rho_out, rho_d, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  int pst = 0;
+  CK(cudaMemcpyAsync(&pst, prep, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (void* p : {(void*)dLam, (void*)dk0k, (void*)lam_d, (void*)k_d, (void*)seg, (void*)val, (void*)raw,
+                  (void*)rho_d, (void*)flags, (void*)nsel, (void*)prep, tmp})
+    cudaFree(p);
+  cudaStreamDestroy(st);
+  if (pst != CV_OK) return fail(CV_ERR_NUMERIC, "non-positive pivot in the Q(Lambda) scale");
+  *block_end = block;
   return CV_OK;
 }
 

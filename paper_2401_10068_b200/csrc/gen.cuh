@@ -61,7 +61,7 @@ struct GenArgs {
 
 // reference model.py:264-265: cov = inverse_batched(Lam); L = cholesky_batched(cov),
 // in the reference's operation order (no FMA contraction).
-__global__ void gen_prep_kernel(const double* Lam, double* Lout, int d, int* status) {
+static __global__ void gen_prep_kernel(const double* Lam, double* Lout, int d, int* status) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double C[kMaxD2];
   *status = CV_OK;

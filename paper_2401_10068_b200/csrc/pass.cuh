@@ -55,6 +55,7 @@ struct PassArgs {
 
 typedef void (*PassFn)(PassArgs);
 struct BatchArgs;
+struct WishartArgs;
 
 struct PassKernel {
   PassFn fn;
@@ -62,6 +63,8 @@ struct PassKernel {
   int smem;  // dynamic shared memory bytes
   void (*tail)(const Hyp*, Ctl*, const double*, int);
   void (*batched)(BatchArgs);
+  void (*wishart_seg)(WishartArgs);
+  void (*wishart_fin)(WishartArgs, const double*, const double*, double, uint64_t, double*, double*);
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

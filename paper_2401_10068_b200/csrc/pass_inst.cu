@@ -2,6 +2,7 @@
 // dimension; the Makefile compiles this file once per CAVI_D in 1..15 so the
 // builds run in parallel.
 #include "batched.cuh"
+#include "posterior.cuh"
 
 #ifndef CAVI_D
 #error "compile with -DCAVI_D=<1..15>"
@@ -19,6 +20,8 @@ static cavi::PassKernel make_kernel() {
   k.smem = G::kSmem;
   k.tail = cavi::tail_kernel<CAVI_D>;
   k.batched = cavi::batched_fit_kernel<CAVI_D>;
+  k.wishart_seg = cavi::wishart_segment_kernel<CAVI_D>;
+  k.wishart_fin = cavi::wishart_finish_kernel<CAVI_D>;
   cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);
   return k;
 }

@@ -299,11 +299,30 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
     return out
 
 
-def vb_posterior_sample(rng, state: VbState, hp, V: int, n_samples: int):
-    """Joint (K, Lambda, rho) draws (reference vb.py:357-393): not on this engine yet."""
+def vb_posterior_sample(rng, state, hp, V: int, n_samples: int):
+    """Joint (K, Lambda, rho) draws from the fitted Q (reference vb.py:357-393), on the GPU.
+
+    Lambda ~ Wishart(n0+V, lam0l_inv^-1) by nu outer products, K | Lambda, rho ~ Gamma,
+    consuming `rng` (an RngStream: seed, stream_id, block cursor `_block`) exactly as the
+    reference does, and advancing its cursor -- same stream position, same draws.
+    Accepts this engine's VbState or any object with a_rho, b_rho, k0k, lam0l_inv.
+    """
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
-    raise NotImplementedError("vb_posterior_sample is the next row of the build (SURVEY 8(f) row 1)")
+    k0k = np.ascontiguousarray(np.atleast_1d(state.k0k), dtype=np.float64)
+    L = np.ascontiguousarray(np.atleast_2d(state.lam0l_inv), dtype=np.float64)
+    d = k0k.shape[0]
+    n = int(n_samples)
+    K = np.empty((n, d))
+    Lam = np.empty((n, d, d))
+    rho = np.empty(n)
+    end = C.c_uint64()
+    _lib.check(_lib.lib().cv_posterior_sample(
+        int(rng.seed) & 0xFFFFFFFFFFFFFFFF, int(rng.stream_id) & 0xFFFFFFFFFFFFFFFF, int(rng._block), d,
+        int(hp.n0), float(hp.q0), int(V), float(state.a_rho), float(state.b_rho), _lib.dptr(k0k), _lib.dptr(L), n,
+        _lib.default_device(), _lib.dptr(K), _lib.dptr(Lam), _lib.dptr(rho), C.byref(end)))
+    rng._block = int(end.value)
+    return {"K": K, "Lambda": Lam, "rho": rho}
 
 
 def install():

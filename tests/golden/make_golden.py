@@ -109,6 +109,20 @@ def save_steps(name, ds, recipe, hp, n_steps=3):
     print(f"{name}: V={ds.V} steps={n_steps} elbo={out['elbo'][-1]!r}")
 
 
+def save_posterior(name, ds, recipe, hp, fit_kw, seed, n, stream_id=0, pre_block=0):
+    """vb_posterior_sample (vb.py:357-393) of the reference's own fitted state."""
+    state, _ = vb.vb_fit(ds, hp, **fit_kw)
+    rng = RngStream(seed, stream_id, pre_block)
+    draws = vb.vb_posterior_sample(rng, state, hp, ds.V, n)
+    recipe = dict(recipe, sha_r=sha(ds.r), sha_mu=sha(ds.mu), sha_D=sha(ds.D))
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), recipe=json.dumps(recipe),
+                        hyper=json.dumps(hyper_recipe(hp)), fit_kw=json.dumps(fit_kw), seed=seed,
+                        stream_id=stream_id, pre_block=pre_block, n=n, end_block=rng._block, V=ds.V,
+                        a_rho=state.a_rho, b_rho=state.b_rho, k0k=state.k0k, lam0l_inv=state.lam0l_inv,
+                        K=draws["K"], Lambda=draws["Lambda"], rho=draws["rho"])
+    print(f"{name}: V={ds.V} n={n} end_block={rng._block}")
+
+
 def main(which=None):
     cases = []
     # config 1: the reference's own test scale, CAVI to convergence
@@ -143,6 +157,16 @@ def main(which=None):
     cases.append(("steps_n3_v30", lambda: (*regime(30, 4, 3), model.default_hyperparams(3))))
     cases.append(("steps_n4_v300", lambda: (*regime(300, 7, 4), model.default_hyperparams(4))))
     cases.append(("steps_n2_v50", lambda: (*regime(50, 3, 2), model.default_hyperparams(2))))
+
+    # posterior draws (vb_posterior_sample): chunked (small nu*d) and one-draw-per-chunk regimes
+    post = [("post_n3_v50", lambda: (*regime(50, 16, 3), model.default_hyperparams(3), {"max_iter": 40}, 91, 500)),
+            ("post_n4_v200", lambda: (*regime(200, 15, 4), model.default_hyperparams(4), {"max_iter": 60}, 7, 300, 3, 11)),
+            ("post_n2_v3000", lambda: (*regime(3000, 4, 2), model.default_hyperparams(2), {"max_iter": 30}, 5, 64)),
+            ("post_n3_v700k", lambda: (*regime(700_000, 2, 3), model.default_hyperparams(3), {"max_iter": 3}, 12, 4))]
+    for name, make in post:
+        if which and name not in which:
+            continue
+        save_posterior(name, *make())
 
     for name, make in cases:
         if which and name not in which:

@@ -92,6 +92,18 @@ def test_direct_oracle_steps_bit_exact(name):
         np.testing.assert_array_equal(st.mu_beta[idx], g["mu_beta"][i])
 
 
+@pytest.mark.parametrize("name", names("post_"))
+def test_posterior_oracle_bit_exact(name):
+    """vb_posterior_sample restated (vb.py:357-393, samplers.py:220-261): same draws, same stream end."""
+    g = Golden(name)
+    s = philox.Stream(int(g["seed"]), int(g["stream_id"]), int(g["pre_block"]))
+    out = cavi.posterior_sample(s, float(g["a_rho"]), float(g["b_rho"]), g["k0k"], g["lam0l_inv"], g.hyper,
+                                int(g["V"]), int(g["n"]))
+    assert s.block == int(g["end_block"])
+    for k in ("K", "Lambda", "rho"):
+        np.testing.assert_array_equal(out[k], g[k])
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_octant_plan_is_world_size_invariant(world):
     r, mu, D, _, _ = philox.make_regime(5000, 3, 4)
