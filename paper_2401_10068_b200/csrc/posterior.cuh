@@ -62,15 +62,9 @@ __global__ void __launch_bounds__(kPostThreads) wishart_segment_kernel(WishartAr
     const uint64_t e0 = ((uint64_t)k * a.nu + row_lo) * D, e1 = ((uint64_t)k * a.nu + row_hi) * D;
     double row[D];
     int j = 0;
-    uint64_t e = e0;
-    if (e & 1) {  // first element is the second half of a block
-      row[j++] = block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1))).y;
-      ++e;
-    }
-    for (; e < e1; e += 2) {
-      const double2 nn = block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1)));
-      row[j++] = nn.x;
-      if (j == D) {
+    auto push = [&](double v) {
+      row[j++] = v;
+      if (j == D) {  // a full row u_i: W += u_i u_i^T
         int p = 0;
 #pragma unroll
         for (int q = 0; q < D; ++q)
@@ -81,20 +75,16 @@ __global__ void __launch_bounds__(kPostThreads) wishart_segment_kernel(WishartAr
           }
         j = 0;
       }
-      if (e + 1 < e1) {
-        row[j++] = nn.y;
-        if (j == D) {
-          int p = 0;
-#pragma unroll
-          for (int q = 0; q < D; ++q)
-#pragma unroll
-            for (int r = q; r < D; ++r) {
-              acc[p] = fma(row[q], row[r], acc[p]);
-              ++p;
-            }
-          j = 0;
-        }
-      }
+    };
+    uint64_t e = e0;
+    if (e & 1) {  // first element is the second half of a block
+      push(block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1))).y);
+      ++e;
+    }
+    for (; e < e1; e += 2) {
+      const double2 nn = block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1)));
+      push(nn.x);
+      if (e + 1 < e1) push(nn.y);
     }
   }
   // fixed-order CTA reduction
