@@ -253,6 +253,165 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
 
 typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
 
+// ---------------------------------------------------------------- d >= 4: fp64 tensor cores
+// mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no fp64 kind).  Per warp and 8 genes:
+//   U = D_8xd A^-1               (s_i = D_i . U_i, t_i = c . D_i, reduced over the 4 lanes of a row)
+//   G += (D o gamma)^T D          (2 k-steps of 4 genes; upper tiles only)
+// Fragments (PTX m8n8k4 .f64): A[r=lane/4][q=lane%4], B[q][r], C[r][2q+i].  A^-1 lives in B
+// fragments (<= 8 doubles/lane), the d x d accumulator in C fragments (<= 6 doubles/lane), so
+// d = 15 fits in registers; padding columns (>= d) are zero.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int D>
+struct MmaConsumer {
+  static constexpr int DP = D <= 8 ? 8 : 16;  // padded dimension
+  static constexpr int NT = DP / 8;           // 8-wide tiles
+  static constexpr int KS = DP / 4;           // k-steps of U = D A^-1
+  static constexpr int NS = n_stats(D);
+  double bfr[NT][KS];   // A^-1[ks*4 + q][nt*8 + r]
+  double cc[NT][2];     // c[nt*8 + 2q + i]
+  double erho;
+  double gacc[NT][NT][2];
+  double gv[NT];
+  double R;
+  LogAcc lg;
+
+  __device__ __forceinline__ void load(const Gen& g, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int row = ks * 4 + q, col = nt * 8 + r;
+        bfr[nt][ks] = (row < D && col < D) ? g.Ainv[row * D + col] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = nt * 8 + 2 * q + i;
+        cc[nt][i] = col < D ? g.c[col] : 0.0;
+      }
+    }
+    erho = g.e_rho;
+  }
+
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt) {
+      gv[mt] = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) gacc[mt][nt][0] = gacc[mt][nt][1] = 0.0;
+    }
+    R = 0.0;
+    lg.init();
+  }
+
+  // genes [gbase, gbase + 8*ngroups) of a stage (x column, then D columns at stride CS)
+  template <typename T, int CS>
+  __device__ __forceinline__ void tile(const T* st, int gbase, int ngroups, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    const T* Dc = st + CS;  // column j at Dc + j*CS
+#pragma unroll 1
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int g0 = gbase + grp * 8;
+      double u[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) u[nt][0] = u[nt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int col = ks * 4 + q;
+        const double av = col < D ? (double)Dc[col * CS + g0 + r] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(u[nt], av, bfr[nt][ks]);
+      }
+      double sp = 0.0, tp = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int col = nt * 8 + 2 * q + i;
+          if (col < D) {
+            const double dv = (double)Dc[col * CS + g0 + r];
+            sp = fma(u[nt][i], dv, sp);
+            tp = fma(cc[nt][i], dv, tp);
+          }
+        }
+      sp += __shfl_xor_sync(0xffffffffu, sp, 1);
+      tp += __shfl_xor_sync(0xffffffffu, tp, 1);
+      sp += __shfl_xor_sync(0xffffffffu, sp, 2);
+      tp += __shfl_xor_sync(0xffffffffu, tp, 2);
+      // per-gene scalars (the 4 lanes of row r hold gene g0 + r)
+      const double x = (double)st[g0 + r];
+      const double den = fma(erho, sp, 1.0);
+      const double inv = ptx::rcp_nr(den);
+      const double xt = x - tp;
+      const double ei = erho * inv;
+      const double w = ei * xt;
+      const double gam = fma(w, w, -ei);
+      const double e = fma(-sp, w, xt);
+      if (q == 0) {
+        R += fma(e, e, sp * inv);
+        lg.mul(den);
+      }
+      // G += (D o gamma)^T D, g += w D over the 8 genes: 2 k-steps of 4 genes
+#pragma unroll
+      for (int ks2 = 0; ks2 < 2; ++ks2) {
+        const int src = (ks2 * 4 + q) * 4;  // a lane holding gene g0 + 4 ks2 + q
+        const double gk = __shfl_sync(0xffffffffu, gam, src);
+        const double wk = __shfl_sync(0xffffffffu, w, src);
+        double dv[NT];
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+          const int col = b * 8 + r;
+          dv[b] = col < D ? (double)Dc[col * CS + g0 + ks2 * 4 + q] : 0.0;
+        }
+#pragma unroll
+        for (int mt = 0; mt < NT; ++mt) {
+          const double av = gk * dv[mt];
+          gv[mt] = fma(wk, dv[mt], gv[mt]);
+#pragma unroll
+          for (int nt = mt; nt < NT; ++nt) dmma(gacc[mt][nt], av, dv[nt]);
+        }
+      }
+    }
+  }
+
+  // this warp's statistic vector [g | G upper | R | Ld] -> out[NS]
+  __device__ __forceinline__ void publish(double* out, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt) {
+      double v = gv[mt];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      const int j = mt * 8 + r;
+      if (q == 0 && j < D) out[j] = v;
+    }
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+      for (int nt = mt; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int j = mt * 8 + r, kk = nt * 8 + 2 * q + i;
+          if (j < D && kk < D && kk >= j) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = gacc[mt][nt][i];
+        }
+    double rv = R, lv = lg.log_value();
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      rv += __shfl_xor_sync(0xffffffffu, rv, off);
+      lv += __shfl_xor_sync(0xffffffffu, lv, off);
+    }
+    if (lane == 0) {
+      out[NS - 2] = rv;
+      out[NS - 1] = lv;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- pipeline geometry
 constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles < kSlots chunks)
 
@@ -280,11 +439,15 @@ struct Geometry {
   static constexpr int kCWarps = kCons / 32;
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
-  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : (D <= 7 ? 512 : 256);  // genes per stage
+  // d <= 3: per-thread register kernel; d >= 4: fp64 tensor-core (DMMA) consumer
+  static constexpr bool kMma = D >= 4;
+  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : 256;  // genes per stage
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
-  static constexpr uint32_t kStageBytes = kColBytes * (1 + D);
+  // smem column stride (elements): +4 doubles for the DMMA fragment loads -> conflict-free banks
+  static constexpr int kColStride = kMma ? kTile + (int)(32 / sizeof(T)) : kTile;
+  static constexpr uint32_t kStageBytes = (uint32_t)kColStride * sizeof(T) * (1 + D);
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   static constexpr int kBudget = CAVI_SMEM_BUDGET - kSlotBytes;
@@ -357,8 +520,8 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
             ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
 #pragma unroll
             for (int j = 0; j < D; ++j)
-              ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kTile, Ds + (int64_t)j * a.Vp + g0, G::kColBytes, &full[stage],
-                            pol);
+              ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kColStride, Ds + (int64_t)j * a.Vp + g0, G::kColBytes,
+                            &full[stage], pol);
           }
           if (++stage == G::kStages) {
             stage = 0;
@@ -372,9 +535,13 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
     return;
   }
 
-  // ---------------- consumers: 8 independent warps, no CTA barrier in the steady state
-  GeneCoef<D> k;
-  load_coef<D>(k, ctl->pass);
+  // ---------------- consumers: independent warps, no CTA barrier in the steady state
+  GeneCoef<(G::kMma ? 1 : D)> k;
+  MmaConsumer<D> mc;
+  if constexpr (G::kMma)
+    mc.load(ctl->pass, lane);
+  else
+    load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&k), ctl->pass);
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
   uint32_t parity = 0;
@@ -383,41 +550,58 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
     ptx::mbar_wait(&full[stage], parity);
     const int64_t chunk = stage_chunk[stage];
     if (chunk < 0) break;
-    double acc[NS];
-#pragma unroll
-    for (int i = 0; i < NS; ++i) acc[i] = 0.0;
-    LogAcc lg;
-    lg.init();
-#pragma unroll 1
-    for (int t = 0; t < G::kTilesPerChunk; ++t) {
-      if (t) ptx::mbar_wait(&full[stage], parity);
-      const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
-      double prod = 1.0;
-#pragma unroll
-      for (int u = 0; u < G::kGenesPerThread; ++u) {
-        const int gi = u * kThreads + tid;
-        double Dv[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) Dv[j] = (double)tile[(j + 1) * G::kTile + gi];
-        prod *= gene<D>(k, (double)tile[gi], Dv, acc);
-      }
-      lg.mul(prod);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[stage]);
-      if (++stage == G::kStages) {
-        stage = 0;
-        parity ^= 1u;
-      }
-    }
-    acc[NS - 1] = lg.log_value();
-    // warp sum (fixed butterfly) -> this warp's slot of the chunk
     double* slot = slots + (size_t)(n_done % kSlots) * kWarps * NS;
+    if constexpr (G::kMma) {
+      mc.reset();
+#pragma unroll 1
+      for (int t = 0; t < G::kTilesPerChunk; ++t) {
+        if (t) ptx::mbar_wait(&full[stage], parity);
+        const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
+        mc.template tile<T, G::kColStride>(tile, warp * (G::kTile / kWarps), G::kTile / kWarps / 8, lane);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+        if (++stage == G::kStages) {
+          stage = 0;
+          parity ^= 1u;
+        }
+      }
+      mc.publish(slot + warp * NS, lane);
+    } else {
+      double acc[NS];
 #pragma unroll
-    for (int i = 0; i < NS; ++i) {
-      double v = acc[i];
+      for (int i = 0; i < NS; ++i) acc[i] = 0.0;
+      LogAcc lg;
+      lg.init();
+#pragma unroll 1
+      for (int t = 0; t < G::kTilesPerChunk; ++t) {
+        if (t) ptx::mbar_wait(&full[stage], parity);
+        const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
+        double prod = 1.0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == (i & 31)) slot[warp * NS + i] = v;
+        for (int u = 0; u < G::kGenesPerThread; ++u) {
+          const int gi = u * kThreads + tid;
+          double Dv[D];
+#pragma unroll
+          for (int j = 0; j < D; ++j) Dv[j] = (double)tile[(j + 1) * G::kColStride + gi];
+          prod *= gene<D>(*reinterpret_cast<const GeneCoef<D>*>(&k), (double)tile[gi], Dv, acc);
+        }
+        lg.mul(prod);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[stage]);
+        if (++stage == G::kStages) {
+          stage = 0;
+          parity ^= 1u;
+        }
+      }
+      acc[NS - 1] = lg.log_value();
+      // warp sum (fixed butterfly) -> this warp's slot of the chunk
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        double v = acc[i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == (i & 31)) slot[warp * NS + i] = v;
+      }
     }
     // the last warp to finish the chunk sums the 8 warp slots (warp order) and carries on up
     unsigned int last = 0;
