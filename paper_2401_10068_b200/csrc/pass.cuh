@@ -448,6 +448,7 @@ struct Geometry {
   // smem column stride (elements): +4 doubles for the DMMA fragment loads -> conflict-free banks
   static constexpr int kColStride = kMma ? kTile + (int)(32 / sizeof(T)) : kTile;
   static constexpr uint32_t kStageBytes = (uint32_t)kColStride * sizeof(T) * (1 + D);
+  static constexpr uint32_t kTxBytes = kColBytes * (1 + D);  // bytes the TMA copies deliver per stage
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   static constexpr int kBudget = CAVI_SMEM_BUDGET - kSlotBytes;
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
             ptx::mbar_arrive(&full[stage]);
           } else {
             stage_chunk[stage] = chunk;
-            ptx::mbar_arrive_expect_tx(&full[stage], G::kStageBytes);
+            ptx::mbar_arrive_expect_tx(&full[stage], G::kTxBytes);
             const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
             T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
             ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
