@@ -261,10 +261,15 @@ typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
 // fragments (<= 8 doubles/lane), the d x d accumulator in C fragments (<= 6 doubles/lane), so
 // d = 15 fits in registers; padding columns (>= d) are zero.
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
+
+#ifndef CAVI_MMA_UNROLL
+#define CAVI_MMA_UNROLL 8
+#endif
+constexpr int kMmaUnroll = CAVI_MMA_UNROLL;  // independent 8-gene groups in flight per warp
 
 template <int D>
 struct MmaConsumer {
@@ -312,9 +317,11 @@ struct MmaConsumer {
   // genes [gbase, gbase + 8*ngroups) of a stage (x column, then D columns at stride CS)
   template <typename T, int CS>
   __device__ __forceinline__ void tile(const T* st, int gbase, int ngroups, int lane) {
+    // branch-free: padding columns (>= D) of the stage are zero, as are the padded fragments
     const int r = lane >> 2, q = lane & 3;
     const T* Dc = st + CS;  // column j at Dc + j*CS
-#pragma unroll 1
+    const bool lead = q == 0;
+#pragma unroll kMmaUnroll
     for (int grp = 0; grp < ngroups; ++grp) {
       const int g0 = gbase + grp * 8;
       double u[NT][2];
@@ -322,8 +329,7 @@ struct MmaConsumer {
       for (int nt = 0; nt < NT; ++nt) u[nt][0] = u[nt][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        const int col = ks * 4 + q;
-        const double av = col < D ? (double)Dc[col * CS + g0 + r] : 0.0;
+        const double av = (double)Dc[(ks * 4 + q) * CS + g0 + r];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) dmma(u[nt], av, bfr[nt][ks]);
       }
@@ -332,12 +338,9 @@ struct MmaConsumer {
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          const int col = nt * 8 + 2 * q + i;
-          if (col < D) {
-            const double dv = (double)Dc[col * CS + g0 + r];
-            sp = fma(u[nt][i], dv, sp);
-            tp = fma(cc[nt][i], dv, tp);
-          }
+          const double dv = (double)Dc[(nt * 8 + 2 * q + i) * CS + g0 + r];
+          sp = fma(u[nt][i], dv, sp);
+          tp = fma(cc[nt][i], dv, tp);
         }
       sp += __shfl_xor_sync(0xffffffffu, sp, 1);
       tp += __shfl_xor_sync(0xffffffffu, tp, 1);
@@ -352,10 +355,8 @@ struct MmaConsumer {
       const double w = ei * xt;
       const double gam = fma(w, w, -ei);
       const double e = fma(-sp, w, xt);
-      if (q == 0) {
-        R += fma(e, e, sp * inv);
-        lg.mul(den);
-      }
+      R += lead ? fma(e, e, sp * inv) : 0.0;
+      lg.mul(lead ? den : 1.0);
       // G += (D o gamma)^T D, g += w D over the 8 genes: 2 k-steps of 4 genes
 #pragma unroll
       for (int ks2 = 0; ks2 < 2; ++ks2) {
@@ -364,10 +365,7 @@ struct MmaConsumer {
         const double wk = __shfl_sync(0xffffffffu, w, src);
         double dv[NT];
 #pragma unroll
-        for (int b = 0; b < NT; ++b) {
-          const int col = b * 8 + r;
-          dv[b] = col < D ? (double)Dc[col * CS + g0 + ks2 * 4 + q] : 0.0;
-        }
+        for (int b = 0; b < NT; ++b) dv[b] = (double)Dc[(b * 8 + r) * CS + g0 + ks2 * 4 + q];
 #pragma unroll
         for (int mt = 0; mt < NT; ++mt) {
           const double av = gk * dv[mt];
@@ -433,21 +431,30 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #define CAVI_MIN_BLOCKS 2  // CTAs per SM
 #endif
 
+#ifndef CAVI_MMA_MIN_D
+#define CAVI_MMA_MIN_D 7  // smallest d served by the DMMA consumer (scalar: 93% HBM at d<=5, 64% at d=6)
+#endif
+#ifndef CAVI_MMA_CONS
+#define CAVI_MMA_CONS 128  // consumer threads per CTA on the DMMA path
+#endif
+
 template <int D, typename T>
 struct Geometry {
-  static constexpr int kCons = CAVI_CONS;
+  static constexpr bool kMma = D >= CAVI_MMA_MIN_D;
+  static constexpr int kCons = kMma ? CAVI_MMA_CONS : CAVI_CONS;
   static constexpr int kCWarps = kCons / 32;
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
-  // d <= 3: per-thread register kernel; d >= 4: fp64 tensor-core (DMMA) consumer
-  static constexpr bool kMma = D >= 4;
-  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : 256;  // genes per stage
+  // small d: per-thread register kernel; larger d: fp64 tensor-core (DMMA) consumer
+  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : (kMma ? 256 : 512);  // genes per stage
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
   // smem column stride (elements): +4 doubles for the DMMA fragment loads -> conflict-free banks
   static constexpr int kColStride = kMma ? kTile + (int)(32 / sizeof(T)) : kTile;
-  static constexpr uint32_t kStageBytes = (uint32_t)kColStride * sizeof(T) * (1 + D);
+  // DMMA path: the stage holds the padded width (8 or 16 columns); columns >= D stay zero
+  static constexpr int kCols = kMma ? (D <= 8 ? 8 : 16) : D;
+  static constexpr uint32_t kStageBytes = (uint32_t)kColStride * sizeof(T) * (1 + kCols);
   static constexpr uint32_t kTxBytes = kColBytes * (1 + D);  // bytes the TMA copies deliver per stage
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
@@ -491,6 +498,12 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
     }
     for (int q = 0; q < kSlots; ++q) s_cnt[q] = 0u;
     ptx::fence_mbar_init();
+  }
+  if constexpr (G::kCols > D) {  // zero the padding columns once: TMA never writes them
+    for (int q = 0; q < G::kStages; ++q) {
+      T* st = stage_base + (size_t)q * (G::kStageBytes / sizeof(T)) + (size_t)(1 + D) * G::kColStride;
+      for (int i = threadIdx.x; i < (G::kCols - D) * G::kColStride; i += blockDim.x) st[i] = (T)0;
+    }
   }
   __syncthreads();
   if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 8] = globaltimer_ns();
