@@ -142,9 +142,21 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
                double param_tol, cv_state* out, double* tr_elbo, double* tr_dk, double* tr_drho,
                double* tr_dlam, int32_t* n_iter);
 /* Per-gene moments of genes [lo, hi) of state `st`; any output may be NULL.
- * mu_beta (n,d), lam_beta (n,d,d), e_bbt (n,d,d), n = hi - lo. */
+ * mu_beta (n,d), lam_beta (n,d,d), e_bbt (n,d,d), sigma = lam_beta^-1 (n,d,d) and the
+ * expected squared residual resid (n) (EM's Sigma, M, S: em.py:22-29), n = hi - lo. */
 int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int64_t lo, int64_t hi,
-                       double* mu_beta, double* lam_beta, double* e_bbt);
+                       double* mu_beta, double* lam_beta, double* e_bbt, double* sigma, double* resid);
+
+/* ---- EM point estimation on the same fused pass (reference em.py) ------- */
+/* em_fit (em.py:97-124) from theta_0 = (K, Lam, rho): one pass per iteration yields the
+ * marginal log-likelihood of theta_n (model.py:278-287) and the E-step sums for
+ * theta_{n+1}.  Traces have room for max_iter entries (tr_K: max_iter x d). */
+int32_t cv_em_fit(cv_dataset* ds, const double* K, const double* Lam, double rho, int32_t max_iter, double rel_tol,
+                  double* K_out, double* Lam_out, double* rho_out, double* tr_loglik, double* tr_K, double* tr_rho,
+                  int32_t* n_iter);
+/* em_step (em.py:80-94): theta -> theta'; optionally Lambda^-1 and ll of the input theta. */
+int32_t cv_em_step(cv_dataset* ds, const double* K, const double* Lam, double rho, double* K_out, double* Lam_out,
+                   double* rho_out, double* Lam_inv_in, double* loglik_in);
 
 /* ---- many independent fits (BASELINE config 4) --------------------------- */
 /* vb_fit on each of n_fits datasets (genes [offsets[f], offsets[f+1]) of r, mu, D),

@@ -49,7 +49,8 @@ LN2PI = np.log(2.0 * np.pi)
 
 
 def n_stats(d: int) -> int:
-    return d + d * (d + 1) // 2 + 2
+    """[g (d) | G upper | R | Q | Ld] -- the device statistic vector."""
+    return d + d * (d + 1) // 2 + 3
 
 
 def triu_index(d: int):
@@ -115,7 +116,7 @@ def gene_terms(x, D, gen: Generator):
     res = (x - t - s * w) ** 2 + s / den
     cols = [w * D[:, j] for j in range(d)]
     cols += [gam * D[:, j] * D[:, k] for j, k in triu_index(d)]
-    cols += [res, np.log(den)]
+    cols += [res, w * (x - t), np.log(den)]
     return np.stack(cols, axis=1)
 
 
@@ -184,7 +185,7 @@ def unpack(stats, d):
     G = np.zeros((d, d))
     for idx, (j, k) in enumerate(triu_index(d)):
         G[j, k] = G[k, j] = stats[d + idx]
-    return g, G, float(stats[-2]), float(stats[-1])
+    return g, G, float(stats[-3]), float(stats[-1])
 
 
 def elbo(stats, gen: Generator, st: Globals, hp: Hyper, V: int) -> float:
@@ -268,7 +269,7 @@ def fit(r, mu, D, hp: Hyper, max_iter=300, rel_tol=1e-8, compute_elbo=True, para
     V = D.shape[0]
     x = r - mu
     gen, st = init(hp, V)
-    resid = float(full_stats(x, D, gen)[-2])
+    resid = float(full_stats(x, D, gen)[-3])
     es, dk, dr, dl = [], [], [], []
     prev = None
     for _ in range(max_iter):
@@ -279,7 +280,7 @@ def fit(r, mu, D, hp: Hyper, max_iter=300, rel_tol=1e-8, compute_elbo=True, para
         dr.append(rel_delta(new.e_rho, st.e_rho))
         dl.append(rel_delta(new.lam0l_inv, st.lam0l_inv))
         st = new
-        resid = float(stats[-2])
+        resid = float(stats[-3])
         if compute_elbo:
             e = elbo(stats, gen, st, hp, V)
             es.append(e)

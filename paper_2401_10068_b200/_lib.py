@@ -81,13 +81,17 @@ _SIGS = {
     "cv_elbo": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
     "cv_fit": (C.c_int32, [C.c_void_p, _P(CvHyper), C.c_int32, C.c_double, C.c_int32, C.c_double, _P(CvState),
                            _D, _D, _D, _D, _P(C.c_int32)]),
-    "cv_materialize": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), C.c_int64, C.c_int64, _D, _D, _D]),
+    "cv_materialize": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), C.c_int64, C.c_int64, _D, _D, _D, _D,
+                                   _D]),
     "cv_nccl_unique_id": (C.c_int32, [C.c_char_p]),
     "cv_comm_create": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "cv_comm_destroy": (None, [C.c_void_p]),
     "cv_dataset_set_comm": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "cv_dataset_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
+    "cv_em_fit": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, C.c_int32, C.c_double, _D, _D, _D, _D, _D, _D,
+                              _P(C.c_int32)]),
+    "cv_em_step": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, _D, _D, _D, _D, _D]),
     "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
                                    C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
     "cv_posterior_sample": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_double,

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kBatchWarps * 32) batched_fit_kernel(BatchArgs
       const double x = __dsub_rn(__ldg(a.r + gi), __ldg(a.mu + gi));  // rm = r - mu (vb.py:149)
       lg.mul(gene<D>(k, x, Dv, acc));
     }
-    acc[NS - 1] = lg.log_value();
+    acc[stat_Ld(D)] = lg.log_value();
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
       double v = acc[i];

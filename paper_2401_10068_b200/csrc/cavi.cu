@@ -341,7 +341,7 @@ int ensure_trace(cv_dataset* ds, int cap) {
   if (ds->trace_cap >= cap) return CV_OK;
   if (ds->trace) CK(cudaFree(ds->trace));
   ds->trace = nullptr;
-  CK(cudaMalloc(&ds->trace, sizeof(double) * 4 * (size_t)cap));
+  CK(cudaMalloc(&ds->trace, sizeof(double) * (4 + kMaxD) * (size_t)cap));  // VB: 4 rows; EM: + K rows
   ds->trace_cap = cap;
   return CV_OK;
 }
@@ -776,8 +776,96 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
   return CV_OK;
 }
 
+// EM shares the fused pass: hyperparameters only carry V for the device constants.
+static int em_setup(cv_dataset* ds, const double* K, const double* Lam, double rho, int max_iter, double rel_tol,
+                    Ctl& c) {
+  if (!(rho > 0)) return fail(CV_ERR_ARG, "rho must be positive");
+  std::vector<double> K0(ds->d, 0.0), L0((size_t)ds->d * ds->d, 0.0);
+  for (int i = 0; i < ds->d; ++i) L0[(size_t)i * ds->d + i] = 1.0;
+  cv_hyper hp{1.0, 1.0, 1.0, 1, ds->d, K0.data(), L0.data()};
+  int rc = upload_hyper(ds, &hp);
+  if (rc) return rc;
+  if ((rc = ensure_trace(ds, std::max(max_iter, 1)))) return rc;
+  reset_ctl(c);
+  c.max_iter = max_iter;
+  c.rel_tol = rel_tol;
+  c.tr_cap = max_iter;
+  c.tr_elbo = ds->trace;
+  c.tr_dk = ds->trace + ds->trace_cap;
+  c.tr_drho = ds->trace + 2 * (size_t)ds->trace_cap;
+  c.tr_dlam = ds->trace + 3 * (size_t)ds->trace_cap;
+  c.tr_k = ds->trace + 4 * (size_t)ds->trace_cap;
+  if ((rc = ctl_put(ds, c))) return rc;
+  double* dp = nullptr;  // theta_0 staged through the hyper block's workspace
+  CK(cudaMalloc(&dp, sizeof(double) * (kMaxD + kMaxD2)));
+  CK(cudaMemcpyAsync(dp, K, sizeof(double) * ds->d, cudaMemcpyHostToDevice, ds->stream));
+  CK(cudaMemcpyAsync(dp + kMaxD, Lam, sizeof(double) * ds->d * ds->d, cudaMemcpyHostToDevice, ds->stream));
+  em_init_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl, dp, dp + kMaxD, rho);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ds->stream));
+  CK(cudaFree(dp));
+  return CV_OK;
+}
+
+int32_t cv_em_fit(cv_dataset* ds, const double* K, const double* Lam, double rho, int32_t max_iter, double rel_tol,
+                  double* K_out, double* Lam_out, double* rho_out, double* tr_loglik, double* tr_K, double* tr_rho,
+                  int32_t* n_iter) {
+  if (!ds || !K || !Lam || !K_out || !Lam_out || !rho_out || !n_iter) return fail(CV_ERR_ARG, "null pointer");
+  if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
+  if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_em_fit on a shard needs cv_dataset_set_comm");
+  Ctl c;
+  int rc = em_setup(ds, K, Lam, rho, max_iter, rel_tol, c);
+  if (rc) return rc;
+  if ((rc = launch_pass(ds))) return rc;  // pass 0: ll(theta_0) + M-step
+  const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
+  if ((rc = ensure_graph(ds, unroll))) return rc;
+  for (int launched = 0;;) {
+    CK(cudaMemcpyAsync(&ds->h_ctl->done, &ds->ctl->done, sizeof(int) * 4, cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaStreamSynchronize(ds->stream));
+    if (ds->h_ctl->done || launched > max_iter) break;
+    CK(cudaGraphLaunch(ds->graph, ds->stream));
+    launched += unroll;
+  }
+  if ((rc = ctl_get(ds))) return rc;
+  const Ctl& h = *ds->h_ctl;
+  if (h.status != CV_OK) return fail(h.status, h.status == CV_ERR_NUMERIC ? "EM step failed: non-positive residual "
+                                                                         "sum or non-PD M-step precision"
+                                                                       : "EM failed (status %d)", h.status);
+  const int d = ds->d;
+  for (int i = 0; i < d; ++i) K_out[i] = h.cur.k0k[i];
+  for (int i = 0; i < d * d; ++i) Lam_out[i] = h.cur.lam0l_inv[i];
+  *rho_out = h.cur.e_rho;
+  const int nit = h.iter - 1;  // M-steps taken
+  *n_iter = nit;
+  if (tr_loglik) CK(cudaMemcpy(tr_loglik, c.tr_elbo, sizeof(double) * nit, cudaMemcpyDeviceToHost));
+  if (tr_rho) CK(cudaMemcpy(tr_rho, c.tr_drho, sizeof(double) * nit, cudaMemcpyDeviceToHost));
+  if (tr_K) CK(cudaMemcpy(tr_K, c.tr_k, sizeof(double) * nit * d, cudaMemcpyDeviceToHost));
+  return CV_OK;
+}
+
+int32_t cv_em_step(cv_dataset* ds, const double* K, const double* Lam, double rho, double* K_out, double* Lam_out,
+                   double* rho_out, double* Lam_inv_in, double* loglik_in) {
+  if (!ds || !K || !Lam || !K_out || !Lam_out || !rho_out) return fail(CV_ERR_ARG, "null pointer");
+  Ctl c;
+  int rc = em_setup(ds, K, Lam, rho, 0x7fffffff, 0.0, c);
+  if (rc) return rc;
+  if ((rc = launch_pass(ds))) return rc;
+  if ((rc = ctl_get(ds))) return rc;
+  const Ctl& h = *ds->h_ctl;
+  if (h.status != CV_OK) return fail(h.status, "EM step failed: non-positive residual sum or non-PD M-step precision");
+  const int d = ds->d;
+  for (int i = 0; i < d; ++i) K_out[i] = h.pass.c[i];
+  for (int i = 0; i < d * d; ++i) {
+    Lam_out[i] = h.pass.A[i];
+    if (Lam_inv_in) Lam_inv_in[i] = h.cur.e_lam[i];
+  }
+  *rho_out = h.pass.e_rho;
+  if (loglik_in) *loglik_in = h.cur.elbo;
+  return CV_OK;
+}
+
 int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int64_t lo, int64_t hi,
-                       double* mu_beta, double* lam_beta, double* e_bbt) {
+                       double* mu_beta, double* lam_beta, double* e_bbt, double* sigma, double* resid) {
   if (!ds || !st) return fail(CV_ERR_ARG, "null pointer");
   if (lo < 0 || hi > ds->V || lo > hi) return fail(CV_ERR_ARG, "bad gene range");
   if (st->d != ds->d) return fail(CV_ERR_ARG, "state does not belong to this dataset");
@@ -790,26 +878,26 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
   c.cur = *st;
   int rc = ctl_put(ds, c);
   if (rc) return rc;
-  double *dm = nullptr, *dl = nullptr, *de = nullptr;
-  if (mu_beta) CK(cudaMalloc(&dm, sizeof(double) * n * d));
-  if (lam_beta) CK(cudaMalloc(&dl, sizeof(double) * n * d * d));
-  if (e_bbt) CK(cudaMalloc(&de, sizeof(double) * n * d * d));
+  double* outs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* hosts[5] = {mu_beta, lam_beta, e_bbt, sigma, resid};
+  const size_t per[5] = {(size_t)d, (size_t)d * d, (size_t)d * d, (size_t)d * d, 1};
+  for (int q = 0; q < 5; ++q)
+    if (hosts[q]) CK(cudaMalloc(&outs[q], sizeof(double) * n * per[q]));
   const int tb = 128;
   const unsigned blocks = (unsigned)((n + tb - 1) / tb);
   if (ds->storage == CV_STORE_F32)
     materialize_kernel<float><<<blocks, tb, 0, ds->stream>>>((const float*)ds->x, (const float*)ds->D, ds->Vp, d, lo, n,
-                                                             ds->ctl, dm, dl, de);
+                                                             ds->ctl, outs[0], outs[1], outs[2], outs[3], outs[4]);
   else
     materialize_kernel<double><<<blocks, tb, 0, ds->stream>>>((const double*)ds->x, (const double*)ds->D, ds->Vp, d, lo,
-                                                              n, ds->ctl, dm, dl, de);
+                                                              n, ds->ctl, outs[0], outs[1], outs[2], outs[3], outs[4]);
   CK(cudaGetLastError());
-  if (dm) CK(cudaMemcpyAsync(mu_beta, dm, sizeof(double) * n * d, cudaMemcpyDeviceToHost, ds->stream));
-  if (dl) CK(cudaMemcpyAsync(lam_beta, dl, sizeof(double) * n * d * d, cudaMemcpyDeviceToHost, ds->stream));
-  if (de) CK(cudaMemcpyAsync(e_bbt, de, sizeof(double) * n * d * d, cudaMemcpyDeviceToHost, ds->stream));
+  for (int q = 0; q < 5; ++q)
+    if (outs[q])
+      CK(cudaMemcpyAsync(hosts[q], outs[q], sizeof(double) * n * per[q], cudaMemcpyDeviceToHost, ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
-  if (dm) CK(cudaFree(dm));
-  if (dl) CK(cudaFree(dl));
-  if (de) CK(cudaFree(de));
+  for (int q = 0; q < 5; ++q)
+    if (outs[q]) CK(cudaFree(outs[q]));
   return CV_OK;
 }
 

@@ -45,6 +45,23 @@ __global__ void state_gen_kernel(Ctl* c, int d) {
   }
 }
 
+// EM: the generator of theta_0 = (K, Lambda, rho) given by the caller (em.py:112-114).
+__global__ void em_init_kernel(Hyp* h, Ctl* c, const double* K, const double* Lam, double rho) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int d = h->d;
+  double ld;
+  for (int i = 0; i < d; ++i) c->pass.c[i] = K[i];
+  for (int i = 0; i < d * d; ++i) c->pass.A[i] = Lam[i];
+  if (!spd_inv_logdet_rt(Lam, c->pass.Ainv, &ld, d, h->wL, h->wJ, h->wM)) {
+    c->status = CV_ERR_NUMERIC;
+    c->done = 1;
+    return;
+  }
+  c->pass.lnA = ld;
+  c->pass.e_rho = rho;
+  c->mode = MODE_EM;
+}
+
 // Per-fit hyperparameter constants and control blocks of a batched fit.
 __global__ void batched_setup_kernel(const Hyp* base, Hyp* hyps, Ctl* ctls, const int64_t* offsets, int64_t n_fits,
                                      int max_iter, double rel_tol, int compute_elbo, double param_tol,

@@ -25,7 +25,7 @@ namespace cavi {
 
 constexpr int kMaxD = CV_MAX_DIM;
 constexpr int kMaxD2 = CV_MAX_D2;
-constexpr int kMaxStats = kMaxD + kMaxD * (kMaxD + 1) / 2 + 2;  // 137
+constexpr int kMaxStats = kMaxD + kMaxD * (kMaxD + 1) / 2 + 3;  // 138
 constexpr int kChunk = 4096;         // genes per chunk (one reduction unit)
 constexpr int kGroupChunks = 64;     // chunks per group
 constexpr int kOctants = 8;          // top of the reduction tree (GPU-count invariant)
@@ -36,7 +36,14 @@ constexpr double kLn2 = 0.69314718055994530942;
 constexpr double kLnPi = 1.14472988584940017414;
 constexpr double kLn2Pi = 1.83787706640934548356;
 
-__host__ __device__ constexpr int n_stats(int d) { return d + d * (d + 1) / 2 + 2; }
+// statistic vector: [ g (d) | G upper (d(d+1)/2) | R | Q | Ld ]
+//   R  = sum (x - t - s w)^2 + s/den   (residual moment sum, vb.py:114-126)
+//   Q  = sum w (x - t) = sum e_rho (x - t)^2 / den   (marginal log-likelihood term, model.py:278-287)
+//   Ld = sum ln den
+__host__ __device__ constexpr int n_stats(int d) { return d + d * (d + 1) / 2 + 3; }
+__host__ __device__ constexpr int stat_R(int d) { return n_stats(d) - 3; }
+__host__ __device__ constexpr int stat_Q(int d) { return n_stats(d) - 2; }
+__host__ __device__ constexpr int stat_Ld(int d) { return n_stats(d) - 1; }
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
@@ -70,7 +77,7 @@ struct Gen {
   double e_rho;
 };
 
-enum { MODE_INIT = 0, MODE_SWEEP = 1, MODE_ELBO = 2 };
+enum { MODE_INIT = 0, MODE_SWEEP = 1, MODE_ELBO = 2, MODE_EM = 3 };
 
 // Control block: current state, the generator of the next pass, fit loop control.
 struct Ctl {
@@ -88,6 +95,7 @@ struct Ctl {
   double* tr_dk;
   double* tr_drho;
   double* tr_dlam;
+  double* tr_k;  // EM: K per iteration [tr_cap][d]
   int tr_cap;
 };
 
@@ -332,8 +340,8 @@ __device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, c
   }
   constexpr int NS = n_stats(D);
   const double V = h.V, nu = h.nu, qv = h.qv;
-  const double R = stats[NS - 2];
-  const double Ld = stats[NS - 1];
+  const double R = stats[stat_R(D)];
+  const double Ld = stats[stat_Ld(D)];
   double G[D * D], Ai[D * D];
   {
     int p = D;
@@ -604,7 +612,7 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
   s.b_rho = b;
   s.e_rho = e_rho;
   s.ln_det_lam0l_inv = ld;
-  s.resid = st[NS - 2];
+  s.resid = st[stat_R(D)];
   s.elbo = elbo;
   s.elbo_status = elbo_status;
   s.gen_lnA = gen.lnA;
@@ -645,11 +653,109 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
       c.pass.Ainv[i] = L[i] * rnu;
     }
     c.pass.lnA = D * h.ln_nu - ld;
-    const double nb = h.b0 + 0.5 * st[NS - 2];
+    const double nb = h.b0 + 0.5 * st[stat_R(D)];
     c.pend_a = h.a_fit;
     c.pend_b = nb;
     c.pass.e_rho = h.a_fit / nb;
   }
+}
+
+// ------------------------------------------------------------------ EM (reference em.py)
+// One pass with the generator theta_n = (K, Lambda, Lambda^-1, rho) yields both
+//   the marginal log-likelihood of theta_n (model.py:278-287):
+//       ll = -1/2 [ V ln 2pi + sum ln den - V ln rho + sum rho (x - t)^2 / den ]   (= Ld, Q)
+//   and the E-step sums of em.py:44-77 for theta_{n+1} (g, G, R exactly as the VB pass).
+// The joint M-step (em.py:80-94), centred:  rho' = V / R,  h = Lambda^-1 g,  K' = K + h / V,
+//   Lambda'^-1 = Lambda^-1 + Lambda^-1 G Lambda^-1 / V - h h^T / V^2 ;  Lambda' = inv(.)
+// Loop bookkeeping of em_fit (em.py:97-124): trace entry n-1 is ll(theta_n); stop when
+// |ll_n - ll_{n-1}| < rel_tol |ll_n| or after max_iter M-steps.
+template <int D>
+__device__ __forceinline__ void em_tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
+  HypT<D> h;
+  h.load(hyp);
+  GenT<D> gen;
+  gen.load(c.pass);
+  cv_state& s = c.cur;
+  const int n = c.iter;
+  const double V = h.V;
+  const double ll = -0.5 * (V * kLn2Pi + stats[stat_Ld(D)] - V * log(gen.e_rho) + stats[stat_Q(D)]);
+  int done = 0;
+  if (n >= 1) {
+    const int it = n - 1;
+    if (it < c.tr_cap) {
+      c.tr_elbo[it] = ll;
+      c.tr_drho[it] = gen.e_rho;
+      for (int j = 0; j < D; ++j) c.tr_k[(size_t)it * D + j] = gen.c[j];
+    }
+    if (fabs(ll - c.prev_elbo) < c.rel_tol * fabs(ll)) done = 1;
+    if (n >= c.max_iter) done = 1;
+  }
+  c.prev_elbo = ll;
+  s.d = D;
+  s.n_iter = n;
+  s.elbo = ll;
+  s.e_rho = gen.e_rho;
+  for (int j = 0; j < D; ++j) s.k0k[j] = gen.c[j];
+  for (int i = 0; i < D * D; ++i) {
+    s.lam0l_inv[i] = gen.A[i];  // EM: the current precision Lambda
+    s.e_lam[i] = gen.Ainv[i];   //     and its inverse
+  }
+  c.iter = n + 1;
+  if (done) {
+    c.done = 1;
+    return;
+  }
+  const double R = stats[stat_R(D)];
+  if (!(R > 0.0) || !isfinite(R)) {  // "non-positive residual sum in M-step" (em.py:85-86)
+    c.status = CV_ERR_NUMERIC;
+    c.done = 1;
+    return;
+  }
+  double G[D * D], hv[D], AG[D * D], Li[D * D], L[D * D], ld;
+  {
+    int p = D;
+    for (int j = 0; j < D; ++j)
+      for (int k = j; k < D; ++k) {
+        G[j * D + k] = stats[p];
+        G[k * D + j] = stats[p];
+        ++p;
+      }
+  }
+  const double* Ai = gen.Ainv;
+  for (int i = 0; i < D; ++i) {
+    double t = 0.0;
+    for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
+    hv[i] = t;
+  }
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) {
+      double t = 0.0;
+      for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
+      AG[i * D + j] = t;
+    }
+  const double rV = 1.0 / V;
+  for (int i = 0; i < D; ++i)
+    for (int j = i; j < D; ++j) {
+      double T = 0.0;
+      for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
+      const double v = 0.5 * (Ai[i * D + j] + Ai[j * D + i]) + T * rV - hv[i] * hv[j] * rV * rV;
+      Li[i * D + j] = v;
+      Li[j * D + i] = v;
+    }
+  if (!spd_inv_logdet_t<D>(Li, L, &ld)) {  // "M-step precision" inversion failed after jitter
+    c.status = CV_ERR_NUMERIC;
+    c.done = 1;
+    return;
+  }
+  for (int i = 0; i < D; ++i) {
+    c.pass.c[i] = gen.c[i] + hv[i] * rV;
+    for (int j = 0; j < D; ++j) {
+      c.pass.A[i * D + j] = 0.5 * (L[i * D + j] + L[j * D + i]);
+      c.pass.Ainv[i * D + j] = Li[i * D + j];
+    }
+  }
+  c.pass.lnA = -ld;
+  c.pass.e_rho = V / R;
 }
 
 }  // namespace cavi

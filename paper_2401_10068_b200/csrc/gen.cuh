@@ -224,10 +224,12 @@ __global__ void download_kernel(const T* xs, const T* Ds, int64_t V, int64_t Vp,
 
 // ------------------------------------------------------------------ per-gene materialisation
 // mu_beta_i = c + w u ; Sigma_i = Ainv - (e_rho/den) u u^T ; lam_beta_i = A + e_rho D D^T ;
-// e_bbt_i = mu mu^T + Sigma_i   (vb.py:150-156)
+// e_bbt_i = mu mu^T + Sigma_i   (vb.py:150-156);  S_i = (x - t - s w)^2 + s/den, the per-gene
+// expected squared residual (em.py:56-60)
 template <typename T>
 __global__ void materialize_kernel(const T* xs, const T* Ds, int64_t Vp, int d, int64_t lo, int64_t n,
-                                   const Ctl* ctl, double* mu_out, double* lam_out, double* ebb_out) {
+                                   const Ctl* ctl, double* mu_out, double* lam_out, double* ebb_out,
+                                   double* sig_out, double* res_out) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int64_t i = lo + k;
@@ -251,9 +253,15 @@ __global__ void materialize_kernel(const T* xs, const T* Ds, int64_t Vp, int d, 
     for (int j = 0; j < d; ++j) mu_out[k * d + j] = m[j];
   for (int j = 0; j < d; ++j)
     for (int q = 0; q < d; ++q) {
+      const double sg = s.gen_Ainv[j * d + q] - (er / den) * u[j] * u[q];
       if (lam_out) lam_out[(k * d + j) * d + q] = s.gen_A[j * d + q] + er * Dv[j] * Dv[q];
-      if (ebb_out) ebb_out[(k * d + j) * d + q] = m[j] * m[q] + (s.gen_Ainv[j * d + q] - (er / den) * u[j] * u[q]);
+      if (ebb_out) ebb_out[(k * d + j) * d + q] = m[j] * m[q] + sg;
+      if (sig_out) sig_out[(k * d + j) * d + q] = sg;
     }
+  if (res_out) {
+    const double e = x - t - sq * w;
+    res_out[k] = e * e + sq / den;
+  }
 }
 
 }  // namespace cavi

@@ -144,7 +144,8 @@ __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const dou
   const double w = ei * xt;
   const double gam = fma(w, w, -ei);
   const double e = fma(-s, w, xt);
-  acc[n_stats(D) - 2] += fma(e, e, s * inv);
+  acc[stat_R(D)] += fma(e, e, s * inv);
+  acc[stat_Q(D)] = fma(w, xt, acc[stat_Q(D)]);
 #pragma unroll
   for (int j = 0; j < D; ++j) acc[j] = fma(w, Dv[j], acc[j]);
 #pragma unroll
@@ -248,7 +249,12 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
     tot[st] = v[0];
   }
   __syncwarp();
-  if (threadIdx.x == 0) tail_t<D>(*h, *c, tot);
+  if (threadIdx.x == 0) {
+    if (c->mode == MODE_EM)
+      em_tail_t<D>(*h, *c, tot);
+    else
+      tail_t<D>(*h, *c, tot);
+  }
 }
 
 typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
@@ -282,7 +288,7 @@ struct MmaConsumer {
   double erho;
   double gacc[NT][NT][2];
   double gv[NT];
-  double R;
+  double R, Q;
   LogAcc lg;
 
   __device__ __forceinline__ void load(const Gen& g, int lane) {
@@ -311,6 +317,7 @@ struct MmaConsumer {
       for (int nt = 0; nt < NT; ++nt) gacc[mt][nt][0] = gacc[mt][nt][1] = 0.0;
     }
     R = 0.0;
+    Q = 0.0;
     lg.init();
   }
 
@@ -356,6 +363,7 @@ struct MmaConsumer {
       const double gam = fma(w, w, -ei);
       const double e = fma(-sp, w, xt);
       R += lead ? fma(e, e, sp * inv) : 0.0;
+      Q += lead ? w * xt : 0.0;
       lg.mul(lead ? den : 1.0);
       // G += (D o gamma)^T D, g += w D over the 8 genes: 2 k-steps of 4 genes
 #pragma unroll
@@ -397,15 +405,17 @@ struct MmaConsumer {
           const int j = mt * 8 + r, kk = nt * 8 + 2 * q + i;
           if (j < D && kk < D && kk >= j) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = gacc[mt][nt][i];
         }
-    double rv = R, lv = lg.log_value();
+    double rv = R, qv = Q, lv = lg.log_value();
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       rv += __shfl_xor_sync(0xffffffffu, rv, off);
+      qv += __shfl_xor_sync(0xffffffffu, qv, off);
       lv += __shfl_xor_sync(0xffffffffu, lv, off);
     }
     if (lane == 0) {
-      out[NS - 2] = rv;
-      out[NS - 1] = lv;
+      out[stat_R(D)] = rv;
+      out[stat_Q(D)] = qv;
+      out[stat_Ld(D)] = lv;
     }
   }
 };
@@ -607,7 +617,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) 
           parity ^= 1u;
         }
       }
-      acc[NS - 1] = lg.log_value();
+      acc[stat_Ld(D)] = lg.log_value();
       // warp sum (fixed butterfly) -> this warp's slot of the chunk
 #pragma unroll
       for (int i = 0; i < NS; ++i) {

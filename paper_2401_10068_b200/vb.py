@@ -141,7 +141,7 @@ class VbState:
             ebb = np.empty((V, d, d))
             hs, keep = _lib.hyper_struct(self._hp)
             _lib.check(_lib.lib().cv_materialize(dds.handle, C.byref(hs), C.byref(self._cs), 0, V,
-                                                 _lib.dptr(mu), _lib.dptr(lam), _lib.dptr(ebb)))
+                                                 _lib.dptr(mu), _lib.dptr(lam), _lib.dptr(ebb), None, None))
             self._lazy.update(mu_beta=self._ro(mu), lam_beta=self._ro(lam), e_bbt=self._ro(ebb))
         return self._lazy
 

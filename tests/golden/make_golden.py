@@ -123,6 +123,24 @@ def save_posterior(name, ds, recipe, hp, fit_kw, seed, n, stream_id=0, pre_block
     print(f"{name}: V={ds.V} n={n} end_block={rng._block}")
 
 
+def save_em(name, ds, recipe, hp, kw):
+    """em.em_fit from the reference CLI's init (K0, Lambda0, rho=1; test_acceptance.py:60)."""
+    from tissuemix import em  # the reference
+
+    init = model.ModelParams(K=hp.K0, Lam=hp.Lambda0, rho=1.0)
+    params, tr = em.em_fit(ds, init, **kw)
+    st = em.em_step(em.EmState(params=init, Sigma=np.empty(0), M=np.empty(0), S=np.empty(0)), ds)
+    idx = subset(ds.V)
+    recipe = dict(recipe, sha_r=sha(ds.r), sha_mu=sha(ds.mu), sha_D=sha(ds.D))
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), recipe=json.dumps(recipe),
+                        hyper=json.dumps(hyper_recipe(hp)), fit_kw=json.dumps(kw),
+                        init_K=hp.K0, init_Lam=hp.Lambda0, init_rho=1.0,
+                        K=params.K, Lam=params.Lam, rho=params.rho, loglik=tr.loglik, tr_K=tr.K, tr_rho=tr.rho,
+                        n_iter=len(tr), step_K=st.params.K, step_Lam=st.params.Lam, step_rho=st.params.rho,
+                        idx=idx, step_Sigma=st.Sigma[idx], step_M=st.M[idx], step_S=st.S[idx])
+    print(f"{name}: V={ds.V} iters={len(tr)} ll={tr.loglik[-1]!r}")
+
+
 def main(which=None):
     cases = []
     # config 1: the reference's own test scale, CAVI to convergence
@@ -167,6 +185,16 @@ def main(which=None):
         if which and name not in which:
             continue
         save_posterior(name, *make())
+
+    ems = [("em_n3_v4000", lambda: (*regime(4000, 404, 3), model.default_hyperparams(3), {})),
+           ("em_n4_v3000", lambda: (*regime(3000, 3, 4), model.default_hyperparams(4), {"max_iter": 300})),
+           ("em_n3_v50", lambda: (*regime(50, 40, 3), model.default_hyperparams(3), {"max_iter": 150})),
+           ("em_n2_v500", lambda: (*regime(500, 8, 2), model.default_hyperparams(2), {"max_iter": 500})),
+           ("em_n8_v2000", lambda: (*regime(2000, 9, 8), model.default_hyperparams(8), {"max_iter": 40}))]
+    for name, make in ems:
+        if which and name not in which:
+            continue
+        save_em(name, *make())
 
     for name, make in cases:
         if which and name not in which:

@@ -104,6 +104,24 @@ def test_posterior_oracle_bit_exact(name):
         np.testing.assert_array_equal(out[k], g[k])
 
 
+@pytest.mark.parametrize("name", names("em_"))
+def test_em_oracle_bit_exact(name):
+    """em_fit / em_step restated (em.py:44-124, model.py:273-287) == the reference's own numbers."""
+    from oracle import em
+
+    g = Golden(name)
+    r, mu, D = g.data()
+    (K, Lam, rho), ll, ks, rhos = em.em_fit(r, mu, D, g["init_K"], g["init_Lam"], float(g["init_rho"]), **g.fit_kw)
+    assert len(ll) == int(g["n_iter"])
+    np.testing.assert_array_equal(ll, g["loglik"])
+    np.testing.assert_array_equal(K, g["K"])
+    np.testing.assert_array_equal(Lam, g["Lam"])
+    assert rho == float(g["rho"])
+    K1, L1, r1, Sig, M, S = em.em_step(r, mu, D, g["init_K"], g["init_Lam"], float(g["init_rho"]))
+    np.testing.assert_array_equal(K1, g["step_K"])
+    np.testing.assert_array_equal(S[g["idx"]], g["step_S"])
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_octant_plan_is_world_size_invariant(world):
     r, mu, D, _, _ = philox.make_regime(5000, 3, 4)
