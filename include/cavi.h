@@ -129,7 +129,8 @@ void cv_comm_destroy(cv_comm* c);
 int32_t cv_dataset_set_comm(cv_dataset* ds, cv_comm* comm);
 /* Mark a shard as rank `rank` of `world` without a communicator (single-GPU
  * emulation of the multi-GPU reduction for tests) and return the shard's
- * octant-subtree statistics of the sweep that would follow state `st`. */
+ * octant-subtree statistics of the sweep that would follow state `st`:
+ * out holds d + d(d+1)/2 + 3 doubles [g | G upper | R | Q | Ld]. */
 int32_t cv_dataset_set_shard(cv_dataset* ds, int32_t rank, int32_t world);
 int32_t cv_shard_stats(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* out);
 

@@ -778,18 +778,18 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
 
 // EM shares the fused pass: hyperparameters only carry V for the device constants.
 static int em_setup(cv_dataset* ds, const double* K, const double* Lam, double rho, int max_iter, double rel_tol,
-                    Ctl& c) {
+                    int trace_cap, Ctl& c) {
   if (!(rho > 0)) return fail(CV_ERR_ARG, "rho must be positive");
   std::vector<double> K0(ds->d, 0.0), L0((size_t)ds->d * ds->d, 0.0);
   for (int i = 0; i < ds->d; ++i) L0[(size_t)i * ds->d + i] = 1.0;
   cv_hyper hp{1.0, 1.0, 1.0, 1, ds->d, K0.data(), L0.data()};
   int rc = upload_hyper(ds, &hp);
   if (rc) return rc;
-  if ((rc = ensure_trace(ds, std::max(max_iter, 1)))) return rc;
+  if ((rc = ensure_trace(ds, std::max(trace_cap, 1)))) return rc;
   reset_ctl(c);
   c.max_iter = max_iter;
   c.rel_tol = rel_tol;
-  c.tr_cap = max_iter;
+  c.tr_cap = trace_cap;
   c.tr_elbo = ds->trace;
   c.tr_dk = ds->trace + ds->trace_cap;
   c.tr_drho = ds->trace + 2 * (size_t)ds->trace_cap;
@@ -814,7 +814,7 @@ int32_t cv_em_fit(cv_dataset* ds, const double* K, const double* Lam, double rho
   if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
   if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_em_fit on a shard needs cv_dataset_set_comm");
   Ctl c;
-  int rc = em_setup(ds, K, Lam, rho, max_iter, rel_tol, c);
+  int rc = em_setup(ds, K, Lam, rho, max_iter, rel_tol, max_iter, c);
   if (rc) return rc;
   if ((rc = launch_pass(ds))) return rc;  // pass 0: ll(theta_0) + M-step
   const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
@@ -847,7 +847,7 @@ int32_t cv_em_step(cv_dataset* ds, const double* K, const double* Lam, double rh
                    double* rho_out, double* Lam_inv_in, double* loglik_in) {
   if (!ds || !K || !Lam || !K_out || !Lam_out || !rho_out) return fail(CV_ERR_ARG, "null pointer");
   Ctl c;
-  int rc = em_setup(ds, K, Lam, rho, 0x7fffffff, 0.0, c);
+  int rc = em_setup(ds, K, Lam, rho, 0x7fffffff, 0.0, 0, c);  // one pass, nothing traced
   if (rc) return rc;
   if ((rc = launch_pass(ds))) return rc;
   if ((rc = ctl_get(ds))) return rc;

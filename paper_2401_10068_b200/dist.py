@@ -1,5 +1,5 @@
 """Multi-GPU CAVI: one process per GPU, genes sharded by octant, one NCCL
-allgather of an n_stats(d)-double partial per sweep (88 bytes at d = 3).
+allgather of an n_stats(d)-double partial per sweep (96 bytes at d = 3).
 
 The reference has no distributed mode (its "parallel" is a thread pool over
 1024-gene chunks with a fixed-tree combine, reference linalg.py:238-255,

@@ -22,6 +22,7 @@ def tree(parts):
 
 @pytest.mark.parametrize("V,N", [(3_000_001, 4), (777_777, 3), (20_000, 6)])
 def test_shard_partials_combine_bit_exact(V, N):
+    from oracle import fused
     from paper_2401_10068_b200 import _lib, dist, model, vb
 
     K, lam = np.full(N - 1, 0.2), np.linalg.inv(0.01 * np.eye(N - 1))
@@ -29,7 +30,7 @@ def test_shard_partials_combine_bit_exact(V, N):
     full = model.generate(9, V, N, K, lam, 100.0)
     st, _ = vb.vb_fit(full, hp, max_iter=4)
     hs, keep = _lib.hyper_struct(hp)
-    ns = (N - 1) + (N - 1) * N // 2 + 2
+    ns = fused.n_stats(N - 1)  # [g | G upper | R | Q | Ld]
 
     def stats(dd, rank, world):
         _lib.check(_lib.lib().cv_dataset_set_shard(dd.handle, rank, world))
