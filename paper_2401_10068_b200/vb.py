@@ -326,7 +326,7 @@ def vb_posterior_sample(rng, state, hp, V: int, n_samples: int):
 
 
 def install():
-    """Rebind the reference's `tissuemix.vb` entry points (and its error types) to this engine.
+    """Rebind the reference's `tissuemix.vb` / `tissuemix.em` entry points (and its error types) to this engine.
 
     After `install()`, `tissuemix.cli` and every caller of `tissuemix.vb.vb_fit`
     run on the GPU; the reference's exception classes are raised so existing
@@ -337,6 +337,12 @@ def install():
 
     linalg.NumericError = ref_linalg.NumericError
     linalg.BatchItemError = ref_linalg.BatchItemError
-    for name in ("vb_init", "vb_step", "vb_elbo", "vb_fit"):
+    for name in ("vb_init", "vb_step", "vb_elbo", "vb_fit", "vb_posterior_sample"):
         setattr(ref_vb, name, globals()[name])
+    import tissuemix.em as ref_em  # noqa: PLC0415
+
+    from . import em  # noqa: PLC0415
+
+    for name in ("em_step", "em_fit"):  # em.py:80-124 (EmState objects are accepted as-is)
+        setattr(ref_em, name, getattr(em, name))
     return ref_vb
