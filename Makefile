@@ -8,7 +8,7 @@ NVFLAGS := -O3 $(ARCH) -lineinfo -std=c++17 $(EXTRA) -Xcompiler -fPIC -Xcompiler
 PKG := paper_2401_10068_b200
 CSRC := $(PKG)/csrc
 BUILD ?= build/obj
-HDR := $(wildcard $(CSRC)/*.cuh) include/cavi.h
+HDR := $(wildcard $(CSRC)/*.cuh) $(CSRC)/pow5_table.inc include/cavi.h
 DIMS := 1 2 3 4 5 6 7 8 9 10 11 12 13 14 15
 PASS_OBJS := $(foreach d,$(DIMS),$(BUILD)/pass_d$(d).o)
 LIB ?= $(PKG)/libcavi.so
@@ -24,8 +24,11 @@ $(BUILD)/pass_d%.o: $(CSRC)/pass_inst.cu $(HDR) | $(BUILD)
 $(BUILD)/cavi.o: $(CSRC)/cavi.cu $(HDR) | $(BUILD)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
-$(LIB): $(BUILD)/cavi.o $(PASS_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib
+$(BUILD)/csv_host.o: $(CSRC)/csv_host.cpp $(CSRC)/numparse.cuh $(CSRC)/pow5_table.inc include/cavi.h | $(BUILD)
+	$(CXX) -O3 -std=c++17 -fPIC -Wall -pthread -c -o $@ $<
+
+$(LIB): $(BUILD)/cavi.o $(BUILD)/csv_host.o $(PASS_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib -Xcompiler -pthread
 
 ptxas: | $(BUILD)
 	$(NVCC) $(NVFLAGS) -DCAVI_D=3 -Xptxas -v -c -o $(BUILD)/ptxas_d3.o $(CSRC)/pass_inst.cu

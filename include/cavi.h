@@ -45,7 +45,8 @@ enum {
   CV_ERR_NONFINITE = 2,
   CV_ERR_ARG = 3,
   CV_ERR_CUDA = 4,
-  CV_ERR_IMPROPER = 5 /* NumericError("Q(Lambda) is improper; dataset too small") */
+  CV_ERR_IMPROPER = 5, /* NumericError("Q(Lambda) is improper; dataset too small") */
+  CV_ERR_FORMAT = 6    /* cli.UsageError: malformed dataset file (header / field count) */
 };
 
 /* storage layouts of the measurement stream in HBM */
@@ -109,8 +110,25 @@ int32_t cv_dataset_create(const double* r, const double* mu, const double* D, in
 int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V_total, int32_t n_networks,
                             const double* K, const double* Lam, double rho, int32_t storage,
                             int32_t device, cv_dataset** out);
+/* ---- dataset files ------------------------------------ */
+/* cli.read_dataset_csv (cli.py:58-75) + model.transform (model.py:174-189): the file body
+ * is copied to HBM and parsed there (one thread per line, Python float() syntax, correctly
+ * rounded) straight into the dataset's stream layout.  Errors as the reference raises them
+ * for the first offending row: CV_ERR_FORMAT (UsageError: header, field count) or
+ * CV_ERR_ARG (ValueError: unparsable / non-finite value, no records). */
+int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, cv_dataset** out,
+                            int32_t* n_networks);
+/* cli.write_dataset_csv (cli.py:47-56): header r,d_1..d_N, rows repr(r), untransformed profile
+ * (D_j + mu, mu), every value formatted exactly as Python's repr(float).  threads <= 0: all cores. */
+int32_t cv_write_dataset_csv(const char* path, const double* r, const double* mu, const double* D, int64_t V,
+                             int32_t d, int32_t threads);
+/* test hooks: the shared decimal parser / repr formatter run on the host
+ * (0 ok, 1 syntax error, 2 needs strtod; repr returns the length written, <= 32 chars) */
+int32_t cv_parse_number_host(const char* s, int64_t n, double* out);
+int32_t cv_format_repr(double x, char* out);
+
 /* Copy back x = r - mu, r, mu and D (row-major) of the shard; any pointer may be
- * NULL (r and mu exist for datasets made by create/generate, which keep them). */
+ * NULL (r and mu exist for datasets made by create/generate/load_csv, which keep them). */
 int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, double* D);
 int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo, int64_t* V_total,
                         int32_t* storage, int64_t* device_bytes);

@@ -16,7 +16,7 @@ from . import linalg
 MAX_D = 15
 MAX_D2 = MAX_D * MAX_D
 
-OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER = range(6)
+OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT = range(7)
 STORE_F64, STORE_F32 = 0, 1
 
 _LIB_PATH = os.environ.get("CAVI_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcavi.so"))
@@ -91,6 +91,10 @@ _SIGS = {
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
     "cv_em_fit": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, C.c_int32, C.c_double, _D, _D, _D, _D, _D, _D,
                               _P(C.c_int32)]),
+    "cv_dataset_load_csv": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, _P(C.c_void_p), _P(C.c_int32)]),
+    "cv_write_dataset_csv": (C.c_int32, [C.c_char_p, _D, _D, _D, C.c_int64, C.c_int32, C.c_int32]),
+    "cv_parse_number_host": (C.c_int32, [C.c_char_p, C.c_int64, _D]),
+    "cv_format_repr": (C.c_int32, [C.c_double, C.c_char_p]),
     "cv_em_step": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, _D, _D, _D, _D, _D]),
     "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
                                    C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
@@ -130,6 +134,10 @@ def lib() -> C.CDLL:
     return _lib
 
 
+class UsageError(ValueError):
+    """A malformed dataset file (the reference's cli.UsageError, cli.py:40-41)."""
+
+
 def check(rc: int) -> None:
     """Map a status code to the reference's exception types (linalg.py:46-69)."""
     if rc == OK:
@@ -141,6 +149,8 @@ def check(rc: int) -> None:
         raise FloatingPointError(msg)
     if rc == ERR_ARG:
         raise ValueError(msg)
+    if rc == ERR_FORMAT:
+        raise UsageError(msg)
     raise RuntimeError(f"libcavi: {msg}")
 
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cerrno>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -12,9 +13,14 @@
 #include <string>
 #include <vector>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include "gen.cuh"
 #include "control.cuh"
 #include "posterior.cuh"
+#include "ingest.cuh"
 
 #include <cub/cub.cuh>
 
@@ -33,6 +39,18 @@ int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
+
+}  // namespace
+
+namespace cavi {
+int set_error(int code, const char* msg);
+}
+int cavi::set_error(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+namespace {
 
 #define CK(call)                                                                                      \
   do {                                                                                                \
@@ -658,6 +676,322 @@ int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, do
   CK(cudaStreamSynchronize(ds->stream));
   if (dx) CK(cudaFree(dx));
   if (dD) CK(cudaFree(dD));
+  return CV_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ dataset CSV reader (ingest.cuh)
+namespace {
+
+std::vector<std::string> split_fields(const std::string& line) {
+  std::vector<std::string> f;
+  size_t a = 0;
+  for (;;) {
+    const size_t b = line.find(',', a);
+    std::string x = line.substr(a, b == std::string::npos ? std::string::npos : b - a);
+    if (x.size() >= 2 && x.front() == '"' && x.back() == '"') x = x.substr(1, x.size() - 2);
+    f.push_back(x);
+    if (b == std::string::npos) break;
+    a = b + 1;
+  }
+  return f;
+}
+
+// a field the device flagged (> 19 significant digits at a rounding boundary): its syntax
+// is already validated, strtod converts the cleaned text with correct rounding
+double slow_value(const std::string& f) {
+  std::string c;
+  for (char ch : f)
+    if (ch != '_' && !num::is_ws(ch)) c.push_back(ch);
+  return std::strtod(c.c_str(), nullptr);
+}
+
+// one row on the host, same rules as row_parse_kernel; -1 when valid
+int host_row(const std::string& line, int N, double* v) {
+  const auto f = split_fields(line);
+  if ((int)f.size() != N + 1) return ingest::kErrFields;
+  int bad_r = 0, bad_d = 0;
+  for (int k = 0; k <= N; ++k) {
+    const int st = num::parse_double(f[k].data(), f[k].data() + f[k].size(), &v[k]);
+    if (st == num::kParseSlow) v[k] = slow_value(f[k]);
+    else if (st == num::kParseBad) (k ? bad_d : bad_r) = 1;
+  }
+  if (bad_r) return ingest::kErrParseR;
+  if (bad_d) return ingest::kErrParseD;
+  for (int j = 1; j <= N; ++j)
+    if (!std::isfinite(v[j])) return ingest::kErrNonfiniteD;
+  if (!std::isfinite(v[0])) return ingest::kErrNonfiniteR;
+  return -1;
+}
+
+int fetch_line(const char* dtext, const int64_t* dterm, int64_t l, std::string* out) {
+  int64_t t2[2] = {-1, 0};
+  if (l > 0) CK(cudaMemcpy(t2, dterm + l - 1, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  else CK(cudaMemcpy(t2 + 1, dterm, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  const int64_t a = t2[0] + 1, b = t2[1];
+  out->assign((size_t)(b > a ? b - a : 0), '\0');
+  if (b > a) CK(cudaMemcpy(&(*out)[0], dtext + a, (size_t)(b - a), cudaMemcpyDeviceToHost));
+  if (!out->empty() && out->back() == '\r') out->pop_back();
+  return CV_OK;
+}
+
+std::string py_str_repr(const std::string& s) { return "'" + s + "'"; }
+
+// the reference's message for the first bad row (cli.py:67-73, model.py:64-86)
+int row_error(const char* path, const std::string& line, int N, int kind) {
+  const auto f = split_fields(line);
+  switch (kind) {
+    case ingest::kErrFields:
+      return fail(CV_ERR_FORMAT, "%s: row has %d fields, expected %d", path, (int)f.size(), N + 1);
+    case ingest::kErrParseR:
+    case ingest::kErrParseD: {
+      double v;
+      for (int k = kind == ingest::kErrParseR ? 0 : 1; k <= N; ++k)
+        if (num::parse_double(f[k].data(), f[k].data() + f[k].size(), &v) == num::kParseBad)
+          return fail(CV_ERR_ARG, "could not convert string to float: %s", py_str_repr(f[k]).c_str());
+      return fail(CV_ERR_ARG, "could not convert string to float");
+    }
+    case ingest::kErrNonfiniteD:
+      return fail(CV_ERR_ARG, "profile contains non-finite entries");
+    default:
+      return fail(CV_ERR_ARG, "expression reading must be finite");
+  }
+}
+
+struct LoadScratch {
+  std::vector<void*> dev;
+  void* pinned[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  int fd = -1;
+  ~LoadScratch() {
+    if (st) cudaStreamSynchronize(st);
+    for (void* p : dev) cudaFree(p);
+    for (int b = 0; b < 2; ++b) {
+      if (pinned[b]) cudaFreeHost(pinned[b]);
+      if (ev[b]) cudaEventDestroy(ev[b]);
+    }
+    if (st) cudaStreamDestroy(st);
+    if (fd >= 0) close(fd);
+  }
+  template <typename P>
+  cudaError_t alloc(P** p, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, bytes ? bytes : 1);
+    if (e == cudaSuccess) dev.push_back(q);
+    *p = (P*)q;
+    return e;
+  }
+};
+
+template <typename T>
+int parse_into(cv_dataset* ds, const char* dtext, const int64_t* dterm, const int64_t* drow, int64_t L, int N,
+               unsigned long long* dkeys, int64_t* dslow, int64_t slow_cap) {
+  const int tb = 256;
+  ingest::row_parse_kernel<T><<<(unsigned)((L + tb - 1) / tb), tb, 0, ds->stream>>>(
+      dtext, dterm, drow, L, N, ds->Vp, ds->r_raw, ds->mu_raw, (T*)ds->x, (T*)ds->D, dkeys, dslow, dkeys + 1,
+      slow_cap);
+  CK(cudaGetLastError());
+  const int64_t pad = ds->Vp - ds->V;
+  if (pad > 0) {
+    CK(cudaMemsetAsync((T*)ds->x + ds->V, 0, sizeof(T) * pad, ds->stream));
+    for (int j = 0; j < ds->d; ++j)
+      CK(cudaMemsetAsync((T*)ds->D + (int64_t)j * ds->Vp + ds->V, 0, sizeof(T) * pad, ds->stream));
+  }
+  return CV_OK;
+}
+
+template <typename T>
+int put_row(cv_dataset* ds, int64_t row, const double* v, int N) {
+  const double mu = v[N];
+  const double r = v[0];
+  const T x = (T)(r - mu);
+  CK(cudaMemcpy(ds->r_raw + row, &r, sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ds->mu_raw + row, &mu, sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy((T*)ds->x + row, &x, sizeof(T), cudaMemcpyHostToDevice));
+  for (int j = 0; j < N - 1; ++j) {
+    const T dj = (T)(v[1 + j] - mu);
+    CK(cudaMemcpy((T*)ds->D + (int64_t)j * ds->Vp + row, &dj, sizeof(T), cudaMemcpyHostToDevice));
+  }
+  return CV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, cv_dataset** out,
+                            int32_t* n_networks) {
+  if (!path || !out) return fail(CV_ERR_ARG, "null pointer");
+  LoadScratch sc;
+  sc.fd = open(path, O_RDONLY);
+  if (sc.fd < 0) return fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  struct stat sb;
+  if (fstat(sc.fd, &sb) != 0) return fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  const int64_t size = (int64_t)sb.st_size;
+  // header = the first line (cli.py:61-64)
+  std::string head;
+  int64_t off = 0;
+  {
+    std::vector<char> buf(1 << 16);
+    bool done = false;
+    while (!done) {
+      const ssize_t n = pread(sc.fd, buf.data(), buf.size(), off);
+      if (n <= 0) break;
+      for (ssize_t i = 0; i < n; ++i) {
+        const char c = buf[i];
+        if (c == '\n' || c == '\r') {
+          off += i + 1;
+          char nx = 0;
+          if (c == '\r' && pread(sc.fd, &nx, 1, off) == 1 && nx == '\n') off += 1;
+          done = true;
+          break;
+        }
+        head.push_back(c);
+      }
+      if (!done) off += n;
+    }
+  }
+  const auto hf = split_fields(head);
+  if (size == 0 || head.empty() || hf[0] != "r" || hf.size() < 3)
+    return fail(CV_ERR_FORMAT, "%s: expected header r,d_1,...,d_N", path);
+  const int N = (int)hf.size() - 1;
+  const int d = N - 1;
+  if (d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
+  const int64_t S0 = size - off;
+  if (S0 <= 0) return fail(CV_ERR_ARG, "no records");
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+  // body -> HBM through two pinned staging buffers (file reads overlap the copies)
+  const int64_t tiles = (S0 + 1 + ingest::kTile - 1) / ingest::kTile;
+  const int64_t Sp = tiles * ingest::kTile;
+  char* dtext = nullptr;
+  CK(sc.alloc(&dtext, (size_t)Sp));
+  CK(cudaMemsetAsync(dtext + S0, 0, (size_t)(Sp - S0), sc.st));
+  const size_t kStage = (size_t)64 << 20;
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaHostAlloc(&sc.pinned[b], kStage, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&sc.ev[b], cudaEventDisableTiming));
+  }
+  char last = 0;
+  for (int64_t pos = 0, k = 0; pos < S0; ++k) {
+    const int b = (int)(k & 1);
+    if (k >= 2) CK(cudaEventSynchronize(sc.ev[b]));
+    const size_t n = (size_t)std::min<int64_t>((int64_t)kStage, S0 - pos);
+    size_t got = 0;
+    while (got < n) {
+      const ssize_t m = pread(sc.fd, (char*)sc.pinned[b] + got, n - got, off + pos + (int64_t)got);
+      if (m <= 0) return fail(CV_ERR_ARG, "%s: short read", path);
+      got += (size_t)m;
+    }
+    last = ((char*)sc.pinned[b])[n - 1];
+    CK(cudaMemcpyAsync(dtext + pos, sc.pinned[b], n, cudaMemcpyHostToDevice, sc.st));
+    CK(cudaEventRecord(sc.ev[b], sc.st));
+    pos += (int64_t)n;
+  }
+  int64_t S = S0;
+  if (last != '\n' && last != '\r') {  // the final line has no terminator: give it one
+    CK(cudaMemsetAsync(dtext + S0, '\n', 1, sc.st));
+    S = S0 + 1;
+  }
+  // 1. line terminators
+  int64_t *tcount = nullptr, *tbase = nullptr;
+  CK(sc.alloc(&tcount, sizeof(int64_t) * tiles));
+  CK(sc.alloc(&tbase, sizeof(int64_t) * tiles));
+  ingest::term_count_kernel<<<(unsigned)tiles, ingest::kTileThreads, 0, sc.st>>>(dtext, S, tcount);
+  CK(cudaGetLastError());
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, tcount, tbase, (int)tiles, sc.st));
+  void* tmp = nullptr;
+  CK(sc.alloc(&tmp, tmp_bytes));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, tcount, tbase, (int)tiles, sc.st));
+  int64_t lastc[2];
+  CK(cudaMemcpyAsync(lastc, tbase + tiles - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+  CK(cudaMemcpyAsync(lastc + 1, tcount + tiles - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+  CK(cudaStreamSynchronize(sc.st));
+  const int64_t L = lastc[0] + lastc[1];
+  if (L > 0x7fffffffll) return fail(CV_ERR_ARG, "%s: more than 2^31 lines", path);
+  int64_t *dterm = nullptr, *dflag = nullptr, *drow = nullptr;
+  CK(sc.alloc(&dterm, sizeof(int64_t) * L));
+  CK(sc.alloc(&dflag, sizeof(int64_t) * L));
+  CK(sc.alloc(&drow, sizeof(int64_t) * L));
+  ingest::term_write_kernel<<<(unsigned)tiles, ingest::kTileThreads, 0, sc.st>>>(dtext, S, tbase, dterm);
+  CK(cudaGetLastError());
+  // 2. rows = non-empty lines, numbered in file order
+  const int tb = 256;
+  ingest::line_flag_kernel<<<(unsigned)((L + tb - 1) / tb), tb, 0, sc.st>>>(dtext, dterm, L, dflag);
+  CK(cudaGetLastError());
+  size_t tmp2 = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, dflag, drow, (int)L, sc.st));
+  void* tmpb = nullptr;
+  CK(sc.alloc(&tmpb, tmp2));
+  CK(cub::DeviceScan::ExclusiveSum(tmpb, tmp2, dflag, drow, (int)L, sc.st));
+  CK(cudaMemcpyAsync(lastc, drow + L - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+  CK(cudaMemcpyAsync(lastc + 1, dflag + L - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.st));
+  CK(cudaStreamSynchronize(sc.st));
+  const int64_t V = lastc[0] + lastc[1];
+  if (V == 0) return fail(CV_ERR_ARG, "no records");  // model.transform (model.py:177-178)
+  // 3. parse straight into the dataset's stream layout
+  cv_dataset* ds = nullptr;
+  int rc = new_dataset(V, d, 0, V, storage, device, &ds);
+  if (rc) return rc;
+  auto bail = [&](int code) {
+    std::string keep = g_err;
+    cv_dataset_destroy(ds);
+    g_err = keep;
+    return code;
+  };
+  if (pool_alloc((void**)&ds->r_raw, sizeof(double) * V, ds->stream, ds->device) != cudaSuccess ||
+      pool_alloc((void**)&ds->mu_raw, sizeof(double) * V, ds->stream, ds->device) != cudaSuccess)
+    return bail(fail(CV_ERR_CUDA, "cudaMalloc raw"));
+  const int64_t slow_cap = std::min<int64_t>(L, 1 << 20);
+  unsigned long long* dkeys = nullptr;
+  int64_t* dslow = nullptr;
+  if (sc.alloc(&dkeys, 2 * sizeof(unsigned long long)) != cudaSuccess || sc.alloc(&dslow, sizeof(int64_t) * slow_cap))
+    return bail(fail(CV_ERR_CUDA, "cudaMalloc"));
+  const unsigned long long init[2] = {~0ull, 0ull};
+  if (cudaMemcpy(dkeys, init, sizeof init, cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(CV_ERR_CUDA, "cudaMemcpy"));
+  rc = storage == CV_STORE_F32 ? parse_into<float>(ds, dtext, dterm, drow, L, N, dkeys, dslow, slow_cap)
+                               : parse_into<double>(ds, dtext, dterm, drow, L, N, dkeys, dslow, slow_cap);
+  if (rc) return bail(rc);
+  unsigned long long keys[2];
+  if (cudaStreamSynchronize(ds->stream) != cudaSuccess ||
+      cudaMemcpy(keys, dkeys, sizeof keys, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return bail(fail(CV_ERR_CUDA, "row parse failed: %s", cudaGetErrorString(cudaGetLastError())));
+  unsigned long long key = keys[0];
+  if (keys[1] > (unsigned long long)slow_cap)
+    return bail(fail(CV_ERR_ARG, "%s: more than %lld numbers with > 19 significant digits", path,
+                     (long long)slow_cap));
+  if (keys[1]) {  // rows with a number the device could not round with certainty
+    std::vector<int64_t> slow((size_t)keys[1]);
+    if (cudaMemcpy(slow.data(), dslow, sizeof(int64_t) * slow.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return bail(fail(CV_ERR_CUDA, "cudaMemcpy"));
+    std::string line;
+    double v[ingest::kMaxFields];
+    for (int64_t l : slow) {
+      if ((rc = fetch_line(dtext, dterm, l, &line))) return bail(rc);
+      const int kind = host_row(line, N, v);
+      if (kind >= 0) {
+        key = std::min(key, ((unsigned long long)l << 3) | (unsigned long long)kind);
+        continue;
+      }
+      int64_t row = 0;
+      if (cudaMemcpy(&row, drow + l, sizeof row, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return bail(fail(CV_ERR_CUDA, "cudaMemcpy"));
+      rc = storage == CV_STORE_F32 ? put_row<float>(ds, row, v, N) : put_row<double>(ds, row, v, N);
+      if (rc) return bail(rc);
+    }
+  }
+  if (key != ~0ull) {
+    std::string line;
+    if ((rc = fetch_line(dtext, dterm, (int64_t)(key >> 3), &line))) return bail(rc);
+    return bail(row_error(path, line, N, (int)(key & 7)));
+  }
+  ds->bad_input = 0;
+  *out = ds;
+  if (n_networks) *n_networks = N;
   return CV_OK;
 }
 
