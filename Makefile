@@ -27,7 +27,10 @@ $(BUILD)/cavi.o: $(CSRC)/cavi.cu $(HDR) | $(BUILD)
 $(BUILD)/csv_host.o: $(CSRC)/csv_host.cpp $(CSRC)/numparse.cuh $(CSRC)/pow5_table.inc include/cavi.h | $(BUILD)
 	$(CXX) -O3 -std=c++17 -fPIC -Wall -pthread -c -o $@ $<
 
-$(LIB): $(BUILD)/cavi.o $(BUILD)/csv_host.o $(PASS_OBJS)
+$(BUILD)/kde.o: $(CSRC)/kde.cu include/cavi.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(LIB): $(BUILD)/cavi.o $(BUILD)/csv_host.o $(BUILD)/kde.o $(PASS_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -cudart static -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib -Xcompiler -pthread
 
 ptxas: | $(BUILD)

@@ -177,6 +177,27 @@ int32_t cv_em_fit(cv_dataset* ds, const double* K, const double* Lam, double rho
 int32_t cv_em_step(cv_dataset* ds, const double* K, const double* Lam, double rho, double* K_out, double* Lam_out,
                    double* rho_out, double* Lam_inv_in, double* loglik_in);
 
+/* ---- posterior summaries (reference analysis.py) -------- */
+/* Per column of `cols` (C columns of n samples, column-major): out[c*10 + k] =
+ * {mean, sd (ddof=1), bandwidth, mode, multimodal, q(qlo), q(qhi), trivial (sd == 0),
+ *  grid lo, grid hi}.  bw[c] > 0 is an explicit bandwidth, else Scott's rule sd * scott
+ * (scott = n ** (-1/5), analysis.py:69-71; zero variance -> CV_ERR_ARG).  range[2c..2c+1]
+ * overrides the grid [min - 4h, max + 4h].  grid_n > 0 evaluates the density on
+ * linspace(lo, hi, grid_n) (grid_out: C x grid_n, optional) and, with find_mode, the
+ * grid argmax + near-tie flag + 3 golden-section steps (kde_mode, analysis.py:98-139). */
+int32_t cv_kde_columns(const double* cols, int64_t n, int32_t C, const double* bw, double scott, double sqrt2pi,
+                       double golden, int32_t grid_n, const double* range, double qlo, double qhi, int32_t find_mode,
+                       int32_t device, double* out, double* grid_out);
+/* kde_density (analysis.py:74-85) at m points. */
+int32_t cv_kde_density(const double* samples, int64_t n, double h, double sqrt2pi, const double* x, int64_t m,
+                       int32_t device, double* out);
+/* summarize (analysis.py:147-188) of n posterior draws K (n x d), rho (n), Lambda (n x d x d,
+ * optional): out[c*10 + k] as cv_kde_columns for the 2d+2 columns K_1..K_d, w_1..w_{d+1}
+ * (full_weights), rho (trivial columns keep mode = first draw); lam_mean: d x d. */
+int32_t cv_summarize(const double* K, const double* rho, const double* Lam, int64_t n, int32_t d, double bandwidth,
+                     double scott, double sqrt2pi, double golden, double qlo, double qhi, int32_t device,
+                     double* out, double* lam_mean);
+
 /* ---- many independent fits (BASELINE config 4) --------------------------- */
 /* vb_fit on each of n_fits datasets (genes [offsets[f], offsets[f+1]) of r, mu, D),
  * all with hyperparameters hp, one warp per fit on `device`.  out: n_fits states;

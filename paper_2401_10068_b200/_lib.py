@@ -95,6 +95,11 @@ _SIGS = {
     "cv_write_dataset_csv": (C.c_int32, [C.c_char_p, _D, _D, _D, C.c_int64, C.c_int32, C.c_int32]),
     "cv_parse_number_host": (C.c_int32, [C.c_char_p, C.c_int64, _D]),
     "cv_format_repr": (C.c_int32, [C.c_double, C.c_char_p]),
+    "cv_kde_columns": (C.c_int32, [_D, C.c_int64, C.c_int32, _D, C.c_double, C.c_double, C.c_double, C.c_int32, _D,
+                                   C.c_double, C.c_double, C.c_int32, C.c_int32, _D, _D]),
+    "cv_kde_density": (C.c_int32, [_D, C.c_int64, C.c_double, C.c_double, _D, C.c_int64, C.c_int32, _D]),
+    "cv_summarize": (C.c_int32, [_D, _D, _D, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double,
+                                 C.c_double, C.c_double, C.c_int32, _D, _D]),
     "cv_em_step": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, _D, _D, _D, _D, _D]),
     "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
                                    C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
