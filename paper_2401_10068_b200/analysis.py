@@ -89,7 +89,8 @@ def kde_density(model: KdeModel, x) -> np.ndarray:
     x = np.ascontiguousarray(np.atleast_1d(np.asarray(x, dtype=np.float64)))
     out = np.empty_like(x)
     flat = x.reshape(-1)
-    _lib.check(_lib.lib().cv_kde_density(_lib.dptr(model.samples), len(model.samples), float(model.bandwidth),
+    smp = np.ascontiguousarray(model.samples, dtype=np.float64)
+    _lib.check(_lib.lib().cv_kde_density(_lib.dptr(smp), len(smp), float(model.bandwidth),
                                          _SQRT2PI, _lib.dptr(flat), flat.shape[0], _dev(), _lib.dptr(out.reshape(-1))))
     return out
 

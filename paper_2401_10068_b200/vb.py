@@ -345,4 +345,14 @@ def install():
 
     for name in ("em_step", "em_fit"):  # em.py:80-124 (EmState objects are accepted as-is)
         setattr(ref_em, name, getattr(em, name))
+    import tissuemix.analysis as ref_an  # noqa: PLC0415
+    import tissuemix.cli as ref_cli  # noqa: PLC0415
+
+    from . import _lib, analysis, ingest  # noqa: PLC0415
+
+    for name in ("kde_fit", "kde_density", "kde_grid", "kde_mode", "summarize"):  # analysis.py:58-188
+        setattr(ref_an, name, getattr(analysis, name))
+    _lib.UsageError = ingest.UsageError = ref_cli.UsageError  # the CLI's `except UsageError` (cli.py:517-519)
+    for name in ("read_dataset_csv", "write_dataset_csv"):  # cli.py:47-75
+        setattr(ref_cli, name, getattr(ingest, name))
     return ref_vb

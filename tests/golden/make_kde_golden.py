@@ -4,7 +4,7 @@ tissuemix.analysis (reference analysis.py:58-188) on seeded inputs.
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_kde_golden.py
 
 Inputs are regenerated in the tests from the recipes below (numpy default_rng seeds,
-or the posterior-draw goldens post_*.npz); tests/golden/kde_expected.npz holds what the
+or the posterior-draw goldens post_*.npz); tests/golden/kde/expected.npz holds what the
 reference returned.
 """
 
@@ -45,7 +45,7 @@ def main():
         rep = analysis.summarize(s, c.get("bw"))
         out[f"{name}/report"] = np.array(json.dumps(rep))
         meta[name] = rep
-    np.savez(os.path.join(HERE, "kde_expected.npz"), **out)
+    np.savez(os.path.join(HERE, "kde", "expected.npz"), **out)
     print(json.dumps(meta, indent=1)[:3000])
 
 

@@ -1,5 +1,5 @@
 """Posterior summaries on the GPU (paper_2401_10068_b200.analysis) against what the
-reference's tissuemix.analysis returned on the same inputs (tests/golden/kde_expected.npz,
+reference's tissuemix.analysis returned on the same inputs (tests/golden/kde/expected.npz,
 made by tests/golden/make_kde_golden.py), plus the reference's own test_analysis.py cases.
 
 Tolerances (fp64): bandwidth, means and densities 1e-12 relative (compensated device sums
@@ -19,7 +19,7 @@ from kde_cases import CASES, SUMMARY_CASES, inputs, summary_inputs
 pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-EXP = np.load(os.path.join(GOLD, "kde_expected.npz"))
+EXP = np.load(os.path.join(GOLD, "kde", "expected.npz"))
 
 
 @pytest.fixture(scope="module")
@@ -37,7 +37,8 @@ def test_kde_matches_reference(an, name):
     assert kde.bandwidth == pytest.approx(float(EXP[f"{name}/bandwidth"]), rel=1e-12)
     n = c.get("grid", 512)
     g = an.kde_grid(kde, lo=c.get("lo"), hi=c.get("hi"), n=n)
-    np.testing.assert_array_equal(g.x, EXP[f"{name}/grid_x"]) if c.get("bw") else None
+    if c.get("bw"):  # same bandwidth bits -> the same linspace
+        np.testing.assert_array_equal(g.x, EXP[f"{name}/grid_x"])
     np.testing.assert_allclose(g.density, EXP[f"{name}/grid_density"], rtol=1e-12, atol=1e-300)
     span = float(EXP[f"{name}/grid_x"][-1] - EXP[f"{name}/grid_x"][0])
     mode, multi = an.kde_mode(kde, n=n, lo=c.get("lo"), hi=c.get("hi"))
