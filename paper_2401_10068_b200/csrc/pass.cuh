@@ -276,14 +276,20 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 #define CAVI_MMA_UNROLL 8
 #endif
 constexpr int kMmaUnroll = CAVI_MMA_UNROLL;  // independent 8-gene groups in flight per warp
+constexpr int kMmaBatchUnroll = kMmaUnroll / 4;  // 4-group batches
 
 template <int D>
 struct MmaConsumer {
   static constexpr int DP = D <= 8 ? 8 : 16;  // padded dimension
-  static constexpr int NT = DP / 8;           // 8-wide tiles
-  static constexpr int KS = DP / 4;           // k-steps of U = D A^-1
+  static constexpr int NT = DP / 8;           // 8-wide output tiles
+  static constexpr int KS = (D + 3) / 4;      // k-steps of Y = D L (rows >= D are zero)
   static constexpr int NS = n_stats(D);
-  double bfr[NT][KS];   // A^-1[ks*4 + q][nt*8 + r]
+  // s = D^T A^-1 D = |L^T D|^2 with A^-1 = L L^T: Y = D L is block lower-triangular, so the
+  // (ks, nt) blocks with 4 ks + 3 < 8 nt vanish.  When d < 8 the free column d of the B
+  // operand carries c, so Y[:, d] = t = D^T c comes out of the same MMAs.
+  static constexpr int kTcol = D < 8 ? D : -1;
+  static constexpr bool live(int ks, int nt) { return 4 * ks + 3 >= 8 * nt || (kTcol >= 0 && nt == 0); }
+  double bfr[NT][KS];   // [L | c][ks*4 + q][nt*8 + r]
   double cc[NT][2];     // c[nt*8 + 2q + i]
   double erho;
   double gacc[NT][NT][2];
@@ -291,21 +297,50 @@ struct MmaConsumer {
   double R, Q;
   LogAcc lg;
 
+  // L = chol(A^-1), warp-cooperative: lane i holds row i (right-looking, one column per
+  // step); then the B fragments are gathered from the row owners.  Runs once per pass,
+  // overlapped with the producer's first TMA loads.
   __device__ __forceinline__ void load(const Gen& g, int lane) {
     const int r = lane >> 2, q = lane & 3;
+    double a[D], l[D];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
+    for (int j = 0; j < D; ++j) {
+      a[j] = lane < D ? g.Ainv[lane * D + j] : 0.0;
+      l[j] = 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const double piv = __shfl_sync(0xffffffffu, a[k], k);
+      const double lkk = sqrt(fmax(piv, 0.0));
+      const double lik = lane == k ? lkk : (lane > k && lane < D ? a[k] / lkk : 0.0);
+      l[k] = lik;
+#pragma unroll
+      for (int j = k + 1; j < D; ++j) {
+        const double ljk = __shfl_sync(0xffffffffu, lik, j);
+        a[j] = fma(-lik, ljk, a[j]);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const int row = ks * 4 + q, col = nt * 8 + r;
-        bfr[nt][ks] = (row < D && col < D) ? g.Ainv[row * D + col] : 0.0;
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double x = __shfl_sync(0xffffffffu, l[c], row < D ? row : 0);
+          if (c == col) v = x;
+        }
+        if (col == kTcol) v = g.c[row < D ? row : 0];
+        bfr[nt][ks] = row < D ? v : 0.0;
       }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int col = nt * 8 + 2 * q + i;
         cc[nt][i] = col < D ? g.c[col] : 0.0;
       }
-    }
     erho = g.e_rho;
   }
 
@@ -321,65 +356,96 @@ struct MmaConsumer {
     lg.init();
   }
 
-  // genes [gbase, gbase + 8*ngroups) of a stage (x column, then D columns at stride CS)
+  // genes [gbase, gbase + 8*ngroups) of a stage (x column, then D columns at stride CS),
+  // in batches of 4 groups (32 genes).  Per batch:
+  //  1. Y = D L per group on the tensor cores (and t = D^T c, see kTcol);
+  //  2. s = sum_k Y_k^2: lane (r, q) holds a partial over its columns; a 4-lane
+  //     reduce-scatter leaves lane (r, q) with the full s, t of gene r of group q, so the
+  //     per-gene scalar chain (den, 1/den, w, gamma, residual) runs once per gene;
+  //  3. G += (D o gamma)^T D on the tensor cores (upper tiles), g += w D.
   template <typename T, int CS>
   __device__ __forceinline__ void tile(const T* st, int gbase, int ngroups, int lane) {
     // branch-free: padding columns (>= D) of the stage are zero, as are the padded fragments
     const int r = lane >> 2, q = lane & 3;
+    const int hi = q >> 1, lo = q & 1;
     const T* Dc = st + CS;  // column j at Dc + j*CS
-    const bool lead = q == 0;
-#pragma unroll kMmaUnroll
-    for (int grp = 0; grp < ngroups; ++grp) {
-      const int g0 = gbase + grp * 8;
-      double u[NT][2];
+#pragma unroll kMmaBatchUnroll
+    for (int b = 0; b < ngroups; b += 4) {
+      const int gb = gbase + b * 8;
+      double sp[4], tp[4];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) u[nt][0] = u[nt][1] = 0.0;
+      for (int g = 0; g < 4; ++g) {
+        const int g0 = gb + g * 8;
+        double u[NT][2];
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const double av = (double)Dc[(ks * 4 + q) * CS + g0 + r];
+        for (int nt = 0; nt < NT; ++nt) u[nt][0] = u[nt][1] = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma(u[nt], av, bfr[nt][ks]);
-      }
-      double sp = 0.0, tp = 0.0;
+        for (int ks = 0; ks < KS; ++ks) {
+          const double av = (double)Dc[(ks * 4 + q) * CS + g0 + r];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double dv = (double)Dc[(nt * 8 + 2 * q + i) * CS + g0 + r];
-          sp = fma(u[nt][i], dv, sp);
-          tp = fma(cc[nt][i], dv, tp);
+          for (int nt = 0; nt < NT; ++nt)
+            if (live(ks, nt)) dmma(u[nt], av, bfr[nt][ks]);
         }
-      sp += __shfl_xor_sync(0xffffffffu, sp, 1);
-      tp += __shfl_xor_sync(0xffffffffu, tp, 1);
-      sp += __shfl_xor_sync(0xffffffffu, sp, 2);
-      tp += __shfl_xor_sync(0xffffffffu, tp, 2);
-      // per-gene scalars (the 4 lanes of row r hold gene g0 + r)
-      const double x = (double)st[g0 + r];
-      const double den = fma(erho, sp, 1.0);
+        double s_ = 0.0, t_ = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int col = nt * 8 + 2 * q + i;
+            if constexpr (kTcol >= 0) {
+              const double y = col == kTcol ? 0.0 : u[nt][i];
+              s_ = fma(y, y, s_);
+              t_ += col == kTcol ? u[nt][i] : 0.0;
+            } else {
+              s_ = fma(u[nt][i], u[nt][i], s_);
+              t_ = fma(cc[nt][i], (double)Dc[col * CS + g0 + r], t_);  // D is zero for col >= D
+            }
+          }
+        sp[g] = s_;
+        tp[g] = t_;
+      }
+      // reduce-scatter over the 4 lanes of row r: lane q keeps group q
+      double s2[2], t2[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double ks_ = hi ? sp[k + 2] : sp[k], kt_ = hi ? tp[k + 2] : tp[k];
+        const double ss_ = hi ? sp[k] : sp[k + 2], st_ = hi ? tp[k] : tp[k + 2];
+        s2[k] = ks_ + __shfl_xor_sync(0xffffffffu, ss_, 2);
+        t2[k] = kt_ + __shfl_xor_sync(0xffffffffu, st_, 2);
+      }
+      const double sv = (lo ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, lo ? s2[0] : s2[1], 1);
+      const double tv = (lo ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, lo ? t2[0] : t2[1], 1);
+      // per-gene scalars: lane (r, q) owns gene gb + 8q + r
+      const double x = (double)st[gb + 8 * q + r];
+      const double den = fma(erho, sv, 1.0);
       const double inv = ptx::rcp_nr(den);
-      const double xt = x - tp;
+      const double xt = x - tv;
       const double ei = erho * inv;
       const double w = ei * xt;
       const double gam = fma(w, w, -ei);
-      const double e = fma(-sp, w, xt);
-      R += lead ? fma(e, e, sp * inv) : 0.0;
-      Q += lead ? w * xt : 0.0;
-      lg.mul(lead ? den : 1.0);
-      // G += (D o gamma)^T D, g += w D over the 8 genes: 2 k-steps of 4 genes
+      const double e = fma(-sv, w, xt);
+      R += fma(e, e, sv * inv);
+      Q += w * xt;
+      lg.mul(den);
+      // G += (D o gamma)^T D, g += w D per group: 2 k-steps of 4 genes
 #pragma unroll
-      for (int ks2 = 0; ks2 < 2; ++ks2) {
-        const int src = (ks2 * 4 + q) * 4;  // a lane holding gene g0 + 4 ks2 + q
-        const double gk = __shfl_sync(0xffffffffu, gam, src);
-        const double wk = __shfl_sync(0xffffffffu, w, src);
-        double dv[NT];
+      for (int g = 0; g < 4; ++g) {
+        const int g0 = gb + g * 8;
 #pragma unroll
-        for (int b = 0; b < NT; ++b) dv[b] = (double)Dc[(b * 8 + r) * CS + g0 + ks2 * 4 + q];
+        for (int ks2 = 0; ks2 < 2; ++ks2) {
+          const int src = (ks2 * 4 + q) * 4 + g;  // the lane owning gene g0 + 4 ks2 + q
+          const double gk = __shfl_sync(0xffffffffu, gam, src);
+          const double wk = __shfl_sync(0xffffffffu, w, src);
+          double dv[NT];
 #pragma unroll
-        for (int mt = 0; mt < NT; ++mt) {
-          const double av = gk * dv[mt];
-          gv[mt] = fma(wk, dv[mt], gv[mt]);
+          for (int bb = 0; bb < NT; ++bb) dv[bb] = (double)Dc[(bb * 8 + r) * CS + g0 + ks2 * 4 + q];
 #pragma unroll
-          for (int nt = mt; nt < NT; ++nt) dmma(gacc[mt][nt], av, dv[nt]);
+          for (int mt = 0; mt < NT; ++mt) {
+            const double av = gk * dv[mt];
+            gv[mt] = fma(wk, dv[mt], gv[mt]);
+#pragma unroll
+            for (int nt = mt; nt < NT; ++nt) dmma(gacc[mt][nt], av, dv[nt]);
+          }
         }
       }
     }
