@@ -272,6 +272,9 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifndef CAVI_HYBRID_MAX_D
+#define CAVI_HYBRID_MAX_D 11  // largest d with the scalar trailing block (d = 12 spills: slower)
+#endif
 #ifndef CAVI_MMA_UNROLL
 #define CAVI_MMA_UNROLL 8
 #endif
@@ -281,7 +284,12 @@ constexpr int kMmaBatchUnroll = kMmaUnroll / 4;  // 4-group batches
 template <int D>
 struct MmaConsumer {
   static constexpr int DP = D <= 8 ? 8 : 16;  // padded dimension
-  static constexpr int NT = DP / 8;           // 8-wide output tiles
+  // 9 <= d <= CAVI_HYBRID_MAX_D: only the 8x8 leading tiles run on the tensor cores; the
+  // RX = d - 8 trailing dimensions (their Y columns and G rows/columns) are cheaper as
+  // per-gene scalar FMAs than as mostly-empty 8x8 tiles
+  static constexpr int RX = (D > 8 && D <= CAVI_HYBRID_MAX_D) ? D - 8 : 0;
+  static constexpr bool kHyb = RX > 0;
+  static constexpr int NT = kHyb ? 1 : DP / 8;  // 8-wide output tiles on the tensor cores
   static constexpr int KS = (D + 3) / 4;      // k-steps of Y = D L (rows >= D are zero)
   static constexpr int NS = n_stats(D);
   // s = D^T A^-1 D = |L^T D|^2 with A^-1 = L L^T: Y = D L is block lower-triangular, so the
@@ -296,6 +304,11 @@ struct MmaConsumer {
   double gv[NT];
   double R, Q;
   LogAcc lg;
+  // hybrid extras (RX > 0): trailing block of L, c; per-lane accumulators of the trailing
+  // G columns (ge: rows < 8, gl: rows >= 8, packed upper) and of g
+  static constexpr int RXa = RX > 0 ? RX : 1;
+  double lx[RXa * (RXa + 1) / 2], cx[RXa];
+  double ge[8][RXa], gl[RXa * (RXa + 1) / 2], gx[RXa];
 
   // L = chol(A^-1), warp-cooperative: lane i holds row i (right-looking, one column per
   // step); then the B fragments are gathered from the row owners.  Runs once per pass,
@@ -341,6 +354,14 @@ struct MmaConsumer {
         const int col = nt * 8 + 2 * q + i;
         cc[nt][i] = col < D ? g.c[col] : 0.0;
       }
+    if constexpr (kHyb) {
+#pragma unroll
+      for (int k = 0; k < RX; ++k) {
+        cx[k] = g.c[8 + k];
+#pragma unroll
+        for (int j = k; j < RX; ++j) lx[j * (j + 1) / 2 + k] = __shfl_sync(0xffffffffu, l[8 + k], 8 + j);
+      }
+    }
     erho = g.e_rho;
   }
 
@@ -354,6 +375,16 @@ struct MmaConsumer {
     R = 0.0;
     Q = 0.0;
     lg.init();
+    if constexpr (kHyb) {
+#pragma unroll
+      for (int k = 0; k < RX; ++k) {
+        gx[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ge[j][k] = 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < RX * (RX + 1) / 2; ++i) gl[i] = 0.0;
+    }
   }
 
   // genes [gbase, gbase + 8*ngroups) of a stage (x column, then D columns at stride CS),
@@ -413,10 +444,25 @@ struct MmaConsumer {
         s2[k] = ks_ + __shfl_xor_sync(0xffffffffu, ss_, 2);
         t2[k] = kt_ + __shfl_xor_sync(0xffffffffu, st_, 2);
       }
-      const double sv = (lo ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, lo ? s2[0] : s2[1], 1);
-      const double tv = (lo ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, lo ? t2[0] : t2[1], 1);
+      const double sv0 = (lo ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, lo ? s2[0] : s2[1], 1);
+      const double tv0 = (lo ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, lo ? t2[0] : t2[1], 1);
       // per-gene scalars: lane (r, q) owns gene gb + 8q + r
-      const double x = (double)st[gb + 8 * q + r];
+      const int own = gb + 8 * q + r;
+      const double x = (double)st[own];
+      double sv = sv0, tv = tv0;
+      double dx[kHyb ? D : 1];
+      if constexpr (kHyb) {  // trailing Y columns and t terms of the own gene
+#pragma unroll
+        for (int j = 0; j < D; ++j) dx[j] = (double)Dc[j * CS + own];
+#pragma unroll
+        for (int k = 0; k < RX; ++k) {
+          double y = 0.0;
+#pragma unroll
+          for (int j = k; j < RX; ++j) y = fma(dx[8 + j], lx[j * (j + 1) / 2 + k], y);
+          sv = fma(y, y, sv);
+          tv = fma(cx[k], dx[8 + k], tv);
+        }
+      }
       const double den = fma(erho, sv, 1.0);
       const double inv = ptx::rcp_nr(den);
       const double xt = x - tv;
@@ -427,6 +473,18 @@ struct MmaConsumer {
       R += fma(e, e, sv * inv);
       Q += w * xt;
       lg.mul(den);
+      if constexpr (kHyb) {  // trailing G columns and g entries of the own gene
+#pragma unroll
+        for (int k = 0; k < RX; ++k) {
+          const double dk = dx[8 + k];
+          gx[k] = fma(w, dk, gx[k]);
+          const double gd = gam * dk;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ge[j][k] = fma(gd, dx[j], ge[j][k]);
+#pragma unroll
+          for (int j = 0; j <= k; ++j) gl[k * (k + 1) / 2 + j] = fma(gd, dx[8 + j], gl[k * (k + 1) / 2 + j]);
+        }
+      }
       // G += (D o gamma)^T D, g += w D per group: 2 k-steps of 4 genes
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -471,6 +529,30 @@ struct MmaConsumer {
           const int j = mt * 8 + r, kk = nt * 8 + 2 * q + i;
           if (j < D && kk < D && kk >= j) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = gacc[mt][nt][i];
         }
+    if constexpr (kHyb) {
+      auto wsum = [](double v) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        return v;
+      };
+#pragma unroll
+      for (int k = 0; k < RX; ++k) {
+        const int kk = 8 + k;
+        const double gs = wsum(gx[k]);
+        if (lane == 0) out[kk] = gs;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double v = wsum(ge[j][k]);
+          if (lane == 0) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = v;
+        }
+#pragma unroll
+        for (int j = 0; j <= k; ++j) {
+          const int jj = 8 + j;
+          const double v = wsum(gl[k * (k + 1) / 2 + j]);
+          if (lane == 0) out[D + jj * D - jj * (jj - 1) / 2 + (kk - jj)] = v;
+        }
+      }
+    }
     double rv = R, qv = Q, lv = lg.log_value();
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -510,6 +592,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_MMA_MIN_D
 #define CAVI_MMA_MIN_D 7  // smallest d served by the DMMA consumer (scalar: 93% HBM at d<=5, 64% at d=6)
 #endif
+#ifndef CAVI_MMA_SMALL_BLOCKS
+#define CAVI_MMA_SMALL_BLOCKS 3  // CTAs per SM for the DMMA consumer at d <= 8
+#endif
 #ifndef CAVI_MMA_CONS
 #define CAVI_MMA_CONS 128  // consumer threads per CTA on the DMMA path
 #endif
@@ -534,7 +619,9 @@ struct Geometry {
   static constexpr uint32_t kTxBytes = kColBytes * (1 + D);  // bytes the TMA copies deliver per stage
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
-  static constexpr int kBudget = CAVI_SMEM_BUDGET - kSlotBytes;
+  // the DMMA kernels at d <= 8 (~110 registers) are latency-bound at 2 CTAs/SM: run 3
+  static constexpr int kMinBlocks = (kMma && D <= 8) ? CAVI_MMA_SMALL_BLOCKS : CAVI_MIN_BLOCKS;
+  static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
   static constexpr int kDrift = (kSlots - 1) * kTilesPerChunk;
   static constexpr int kStages = kFit < 8 ? (kFit < kDrift ? kFit : kDrift) : (8 < kDrift ? 8 : kDrift);
@@ -549,7 +636,7 @@ struct Geometry {
 };
 
 template <int D, typename T>
-__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, CAVI_MIN_BLOCKS) pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::kMinBlocks) pass_kernel(PassArgs a) {
   using G = Geometry<D, T>;
   constexpr int NS = n_stats(D);
   constexpr int kWarps = G::kCWarps;
