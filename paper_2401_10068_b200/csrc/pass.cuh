@@ -290,6 +290,11 @@ struct MmaConsumer {
   static constexpr int RX = (D > 8 && D <= CAVI_HYBRID_MAX_D) ? D - 8 : 0;
   static constexpr bool kHyb = RX > 0;
   static constexpr int NT = kHyb ? 1 : DP / 8;  // 8-wide output tiles on the tensor cores
+  // d > CAVI_HYBRID_MAX_D: Y and the G tiles of rows < 8 on the tensor cores, the trailing
+  // diagonal block of G (and g) as per-gene scalar FMAs instead of the 8x8 tile (1, 1)
+  static constexpr bool kSemi = D > 8 && !kHyb;
+  static constexpr int RT = (kHyb || kSemi) ? D - 8 : 0;  // trailing dimensions done in scalar
+  static constexpr int MTG = kSemi ? 1 : NT;              // G row tiles on the tensor cores
   static constexpr int KS = (D + 3) / 4;      // k-steps of Y = D L (rows >= D are zero)
   static constexpr int NS = n_stats(D);
   // s = D^T A^-1 D = |L^T D|^2 with A^-1 = L L^T: Y = D L is block lower-triangular, so the
@@ -306,9 +311,9 @@ struct MmaConsumer {
   LogAcc lg;
   // hybrid extras (RX > 0): trailing block of L, c; per-lane accumulators of the trailing
   // G columns (ge: rows < 8, gl: rows >= 8, packed upper) and of g
-  static constexpr int RXa = RX > 0 ? RX : 1;
+  static constexpr int RXa = RX > 0 ? RX : 1, RTa = RT > 0 ? RT : 1;
   double lx[RXa * (RXa + 1) / 2], cx[RXa];
-  double ge[8][RXa], gl[RXa * (RXa + 1) / 2], gx[RXa];
+  double ge[8][RXa], gl[RTa * (RTa + 1) / 2], gx[RTa];
 
   // L = chol(A^-1), warp-cooperative: lane i holds row i (right-looking, one column per
   // step); then the B fragments are gathered from the row owners.  Runs once per pass,
@@ -375,15 +380,15 @@ struct MmaConsumer {
     R = 0.0;
     Q = 0.0;
     lg.init();
+#pragma unroll
+    for (int k = 0; k < RT; ++k) gx[k] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RT * (RT + 1) / 2; ++i) gl[i] = 0.0;
     if constexpr (kHyb) {
 #pragma unroll
-      for (int k = 0; k < RX; ++k) {
-        gx[k] = 0.0;
+      for (int k = 0; k < RX; ++k)
 #pragma unroll
         for (int j = 0; j < 8; ++j) ge[j][k] = 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < RX * (RX + 1) / 2; ++i) gl[i] = 0.0;
     }
   }
 
@@ -450,10 +455,12 @@ struct MmaConsumer {
       const int own = gb + 8 * q + r;
       const double x = (double)st[own];
       double sv = sv0, tv = tv0;
-      double dx[kHyb ? D : 1];
-      if constexpr (kHyb) {  // trailing Y columns and t terms of the own gene
+      double dx[RT > 0 ? D : 1];
+      if constexpr (RT > 0) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) dx[j] = (double)Dc[j * CS + own];
+        for (int j = kHyb ? 0 : 8; j < D; ++j) dx[j] = (double)Dc[j * CS + own];
+      }
+      if constexpr (kHyb) {  // trailing Y columns and t terms of the own gene
 #pragma unroll
         for (int k = 0; k < RX; ++k) {
           double y = 0.0;
@@ -473,14 +480,16 @@ struct MmaConsumer {
       R += fma(e, e, sv * inv);
       Q += w * xt;
       lg.mul(den);
-      if constexpr (kHyb) {  // trailing G columns and g entries of the own gene
+      if constexpr (RT > 0) {  // trailing G block (and g entries) of the own gene
 #pragma unroll
-        for (int k = 0; k < RX; ++k) {
+        for (int k = 0; k < RT; ++k) {
           const double dk = dx[8 + k];
           gx[k] = fma(w, dk, gx[k]);
           const double gd = gam * dk;
+          if constexpr (kHyb) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ge[j][k] = fma(gd, dx[j], ge[j][k]);
+            for (int j = 0; j < 8; ++j) ge[j][k] = fma(gd, dx[j], ge[j][k]);
+          }
 #pragma unroll
           for (int j = 0; j <= k; ++j) gl[k * (k + 1) / 2 + j] = fma(gd, dx[8 + j], gl[k * (k + 1) / 2 + j]);
         }
@@ -498,7 +507,7 @@ struct MmaConsumer {
 #pragma unroll
           for (int bb = 0; bb < NT; ++bb) dv[bb] = (double)Dc[(bb * 8 + r) * CS + g0 + ks2 * 4 + q];
 #pragma unroll
-          for (int mt = 0; mt < NT; ++mt) {
+          for (int mt = 0; mt < MTG; ++mt) {
             const double av = gk * dv[mt];
             gv[mt] = fma(wk, dv[mt], gv[mt]);
 #pragma unroll
@@ -513,7 +522,7 @@ struct MmaConsumer {
   __device__ __forceinline__ void publish(double* out, int lane) {
     const int r = lane >> 2, q = lane & 3;
 #pragma unroll
-    for (int mt = 0; mt < NT; ++mt) {
+    for (int mt = 0; mt < MTG; ++mt) {
       double v = gv[mt];
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       v += __shfl_xor_sync(0xffffffffu, v, 2);
@@ -521,7 +530,7 @@ struct MmaConsumer {
       if (q == 0 && j < D) out[j] = v;
     }
 #pragma unroll
-    for (int mt = 0; mt < NT; ++mt)
+    for (int mt = 0; mt < MTG; ++mt)
 #pragma unroll
       for (int nt = mt; nt < NT; ++nt)
 #pragma unroll
@@ -529,20 +538,20 @@ struct MmaConsumer {
           const int j = mt * 8 + r, kk = nt * 8 + 2 * q + i;
           if (j < D && kk < D && kk >= j) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = gacc[mt][nt][i];
         }
-    if constexpr (kHyb) {
+    if constexpr (RT > 0) {
       auto wsum = [](double v) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         return v;
       };
 #pragma unroll
-      for (int k = 0; k < RX; ++k) {
+      for (int k = 0; k < RT; ++k) {
         const int kk = 8 + k;
         const double gs = wsum(gx[k]);
         if (lane == 0) out[kk] = gs;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const double v = wsum(ge[j][k]);
+        for (int j = 0; j < (kHyb ? 8 : 0); ++j) {
+          const double v = wsum(ge[j][k < RX ? k : 0]);
           if (lane == 0) out[D + j * D - j * (j - 1) / 2 + (kk - j)] = v;
         }
 #pragma unroll
