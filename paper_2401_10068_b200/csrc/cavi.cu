@@ -1257,14 +1257,15 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
   int64_t* doff;
   Hyp *base, *hyps;
   Ctl* ctls;
-  CK(cudaMalloc(&dr, sizeof(double) * G));
-  CK(cudaMalloc(&dmu, sizeof(double) * G));
-  CK(cudaMalloc(&dD, sizeof(double) * G * d));
-  CK(cudaMalloc(&doff, sizeof(int64_t) * (n_fits + 1)));
-  CK(cudaMalloc(&base, sizeof(Hyp)));
-  CK(cudaMalloc(&hyps, sizeof(Hyp) * n_fits));
-  CK(cudaMalloc(&ctls, sizeof(Ctl) * n_fits));
-  CK(cudaMalloc(&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits));
+  // stream-ordered pool allocations: repeated batches reuse the HBM (release threshold max)
+  CK(pool_alloc((void**)&dr, sizeof(double) * G, st, device));
+  CK(pool_alloc((void**)&dmu, sizeof(double) * G, st, device));
+  CK(pool_alloc((void**)&dD, sizeof(double) * G * d, st, device));
+  CK(pool_alloc((void**)&doff, sizeof(int64_t) * (n_fits + 1), st, device));
+  CK(pool_alloc((void**)&base, sizeof(Hyp), st, device));
+  CK(pool_alloc((void**)&hyps, sizeof(Hyp) * n_fits, st, device));
+  CK(pool_alloc((void**)&ctls, sizeof(Ctl) * n_fits, st, device));
+  CK(pool_alloc((void**)&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, st, device));
   CK(cudaMemcpyAsync(dr, r, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * G * d, cudaMemcpyHostToDevice, st));
@@ -1286,8 +1287,8 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
                                           param_tol, dtr);
   CK(cudaGetLastError());
   BatchArgs a{dr, dmu, dD, doff, n_fits, hyps, ctls};
-  const unsigned nb = (unsigned)((n_fits + kBatchWarps - 1) / kBatchWarps);
-  pk.batched<<<nb, kBatchWarps * 32, 0, st>>>(a);
+  const unsigned nb = (unsigned)((n_fits + kBatchThreads - 1) / kBatchThreads);
+  pk.batched<<<nb, kBatchThreads, 0, st>>>(a);
   CK(cudaGetLastError());
   // states are the first member of each control block: one strided copy
   CK(cudaMemcpy2DAsync(out, sizeof(cv_state), ctls, sizeof(Ctl), sizeof(cv_state), n_fits, cudaMemcpyDeviceToHost,
@@ -1297,9 +1298,9 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
   std::vector<int> status(n_fits);
   CK(cudaMemcpy2DAsync(status.data(), sizeof(int), &ctls[0].status, sizeof(Ctl), sizeof(int), n_fits,
                        cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   for (void* p : {(void*)dr, (void*)dmu, (void*)dD, (void*)doff, (void*)base, (void*)hyps, (void*)ctls, (void*)dtr})
-    cudaFree(p);
+    cudaFreeAsync(p, st);
+  CK(cudaStreamSynchronize(st));
   cudaStreamDestroy(st);
   for (int64_t f = 0; f < n_fits; ++f) {
     if (status[f] == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "fit %lld: Q(Lambda) is improper; dataset too small", (long long)f);

@@ -599,7 +599,7 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #endif
 
 #ifndef CAVI_MMA_MIN_D
-#define CAVI_MMA_MIN_D 7  // smallest d served by the DMMA consumer (scalar: 93% HBM at d<=5, 64% at d=6)
+#define CAVI_MMA_MIN_D 6  // smallest d served by the DMMA consumer (scalar d=6 spills: 424 vs 704 sweeps/s)
 #endif
 #ifndef CAVI_MMA_SMALL_BLOCKS
 #define CAVI_MMA_SMALL_BLOCKS 3  // CTAs per SM for the DMMA consumer at d <= 8

@@ -24,6 +24,7 @@ fixed deterministic tree, so results never depend on worker or GPU count.
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Sequence
 import weakref
 from dataclasses import dataclass
 
@@ -259,8 +260,8 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
                 param_tol: float = 1e-10, device: int | None = None):
     """vb_fit on many independent datasets at once (BASELINE config 4: tissue samples).
 
-    One warp per fit runs the whole CAVI loop in-kernel (csrc/batched.cuh).  Returns a
-    list of (VbState, VbTrace), each equal to what vb_fit(ds, hp, ...) returns for
+    One thread per fit runs the whole CAVI loop in-kernel (csrc/batched.cuh).  Returns a
+    sequence of (VbState, VbTrace), each equal to what vb_fit(ds, hp, ...) returns for
     that dataset (within 1e-9, same iteration count).  The datasets must share N.
     """
     datasets = list(datasets)
@@ -268,19 +269,24 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
         raise ValueError("no datasets")
     if max_iter < 1:
         raise ValueError("max_iter must be >= 1")
-    Ds = [np.ascontiguousarray(np.atleast_2d(ds.D), dtype=np.float64) for ds in datasets]
-    d = Ds[0].shape[1]
-    if any(Dm.shape[1] != d for Dm in Ds):
+    # one concatenation per field (no per-dataset conversions: 1e4-1e5 datasets per call)
+    try:
+        D = np.ascontiguousarray(np.concatenate([ds.D for ds in datasets], axis=0), dtype=np.float64)
+    except ValueError:
+        raise ValueError("all datasets must have the same number of networks") from None
+    if D.ndim != 2:
         raise ValueError("all datasets must have the same number of networks")
+    d = D.shape[1]
     hd = int(np.atleast_1d(hp.K0).shape[0])
     if hd != d:
         raise ValueError(f"hyperparams dim {hd} != dataset dim {d}")
-    r = np.ascontiguousarray(np.concatenate([np.atleast_1d(ds.r) for ds in datasets]), dtype=np.float64)
-    mu = np.ascontiguousarray(np.concatenate([np.atleast_1d(ds.mu) for ds in datasets]), dtype=np.float64)
-    D = np.ascontiguousarray(np.concatenate(Ds, axis=0))
-    offsets = np.zeros(len(datasets) + 1, dtype=np.int64)
-    offsets[1:] = np.cumsum([Dm.shape[0] for Dm in Ds])
+    r = np.ascontiguousarray(np.concatenate([ds.r for ds in datasets]), dtype=np.float64)
+    mu = np.ascontiguousarray(np.concatenate([ds.mu for ds in datasets]), dtype=np.float64)
     n = len(datasets)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.fromiter((len(ds.r) for ds in datasets), dtype=np.int64, count=n), out=offsets[1:])
+    if offsets[-1] != D.shape[0] or r.shape[0] != D.shape[0]:
+        raise ValueError("r, mu and D of a dataset must have the same number of genes")
     states = (_lib.CvState * n)()
     tr = np.empty((n, 4, max_iter))
     hs, keep = _lib.hyper_struct(hp)
@@ -288,15 +294,42 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
         _lib.dptr(r), _lib.dptr(mu), _lib.dptr(D), offsets.ctypes.data_as(C.POINTER(C.c_int64)), n, d,
         C.byref(hs), int(max_iter), float(rel_tol), int(bool(compute_elbo)), float(param_tol),
         _lib.default_device() if device is None else device, states, _lib.dptr(tr)))
-    out = []
-    for f, ds in enumerate(datasets):
-        cs = states[f].copy()
-        k = int(cs.n_iter)
-        st = VbState(cs, None, hp)
-        st._lazy["source"] = ds
-        out.append((st, VbTrace(elbo=tr[f, 0, :k].copy(), delta_k0k=tr[f, 1, :k].copy(),
-                                delta_rho=tr[f, 2, :k].copy(), delta_lam=tr[f, 3, :k].copy())))
-    return out
+    raw = np.frombuffer(states, dtype=np.uint8).reshape(n, C.sizeof(_lib.CvState))
+    off = _lib.CvState.n_iter.offset
+    n_iter = raw[:, off:off + 4].copy().view(np.int32)[:, 0]
+    return FitBatch(datasets, states, tr, n_iter, hp)
+
+
+class FitBatch(Sequence):
+    """The (VbState, VbTrace) pairs of a vb_fit_many call, built on access.
+
+    Each state is a view of its slot in the batch's state buffer and each trace a view
+    of its rows in the trace buffer (no per-fit copies: 1e4-1e5 fits per call).
+    """
+
+    def __init__(self, datasets, states, tr, n_iter, hp):
+        self._ds, self._states, self._tr, self._n_iter, self._hp = datasets, states, tr, n_iter, hp
+
+    def __len__(self) -> int:
+        return len(self._ds)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        st = VbState(self._states[i], None, self._hp)
+        st._lazy["source"] = self._ds[i]
+        k = int(self._n_iter[i])
+        t = self._tr[i]
+        return st, VbTrace(elbo=t[0, :k], delta_k0k=t[1, :k], delta_rho=t[2, :k], delta_lam=t[3, :k])
+
+    @property
+    def n_iter(self) -> np.ndarray:
+        """Iterations per fit (no per-fit objects needed)."""
+        return self._n_iter
 
 
 def vb_posterior_sample(rng, state, hp, V: int, n_samples: int):
