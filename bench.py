@@ -197,7 +197,7 @@ def run_ours(args):
     if world != 1 or args.gpus != 1 or args.force_dist:
         from paper_2401_10068_b200 import dist  # noqa: PLC0415
 
-        return dist.bench_main(args, METRIC, UNIT)
+        return dist.bench_main(args, METRIC, UNIT, clocks_cls=Clocks)
 
     dev = _lib.default_device()
     V, N = int(args.genes), args.networks

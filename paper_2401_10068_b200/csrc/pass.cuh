@@ -591,6 +591,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_TILE_SMALL_D
 #define CAVI_TILE_SMALL_D 1024  // genes per stage for d <= 3
 #endif
+#ifndef CAVI_TILE_TINY_D
+#define CAVI_TILE_TINY_D 2048  // genes per stage for d = 1 (N=2: 3116 -> 3291 sweeps/s)
+#endif
 #ifndef CAVI_SMEM_BUDGET
 #define CAVI_SMEM_BUDGET 100000
 #endif
@@ -616,7 +619,7 @@ struct Geometry {
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
   // small d: per-thread register kernel; larger d: fp64 tensor-core (DMMA) consumer
-  static constexpr int kTile = D <= 3 ? CAVI_TILE_SMALL_D : (kMma ? 256 : 512);  // genes per stage
+  static constexpr int kTile = D <= 1 ? CAVI_TILE_TINY_D : D <= 3 ? CAVI_TILE_SMALL_D : (kMma ? 256 : 512);  // genes/stage
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);

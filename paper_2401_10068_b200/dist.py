@@ -152,8 +152,13 @@ def shard_upload(ds, comm: Comm, storage: str = "f64", V_total: int | None = Non
 
 
 # ---------------------------------------------------------------------------- bench leg
-def bench_main(args, metric: str, unit: str) -> int:
-    """bench.py at N>1: strong scaling of the V-gene sweep over the ranks of torchrun."""
+def bench_main(args, metric: str, unit: str, clocks_cls=None) -> int:
+    """bench.py at N>1: strong scaling of the V-gene sweep over the ranks of torchrun.
+
+    Device-timed sweeps (max over ranks), nvidia-smi clocks during them (rank 0's GPU),
+    and the end-to-end public call at N GPUs: each rank uploads its shard from pinned
+    host memory and runs vb.vb_fit on it with the communicator attached (max over ranks).
+    """
     import torch  # noqa: PLC0415
 
     from . import vb  # noqa: PLC0415
@@ -173,14 +178,25 @@ def bench_main(args, metric: str, unit: str) -> int:
     hs, keep = _lib.hyper_struct(hp)
     ms_total, ms_kernel, nl = C.c_double(), C.c_double(), C.c_int32()
     td.barrier()
+    clk = clocks_cls(local) if clocks_cls is not None else None
+    if clk is not None:
+        clk.__enter__()
     _lib.check(_lib.lib().cv_bench_sweeps(shard.handle, C.byref(hs), C.byref(st._cs), args.warmup, args.steps,
                                           C.byref(ms_total), C.byref(ms_kernel), C.byref(nl)))
+    td.barrier()
     t = torch.tensor([ms_total.value, ms_kernel.value], dtype=torch.float64)
     td.all_reduce(t, op=td.ReduceOp.MAX)
     ms_step = float(t[0]) / args.steps
+    if clk is not None:
+        # keep the clocks sampler running over >= 1 s of the same sweeps (same count on every rank)
+        soak = 0 if getattr(args, "profile", False) else max(0, int(1000.0 / max(ms_step, 1e-3)) - args.steps)
+        if soak:
+            a_, b_, c_ = C.c_double(), C.c_double(), C.c_int32()
+            _lib.check(_lib.lib().cv_bench_sweeps(shard.handle, C.byref(hs), C.byref(st._cs), 0, min(soak, 20000),
+                                                  C.byref(a_), C.byref(b_), C.byref(c_)))
+        clk.__exit__(None, None, None)
     kern_s = float(t[1]) / args.steps / 1e3
     esz = 8 if args.storage == "f64" else 4
-    lo, hi = shard_ranges(V, world)[rank]
     peak = 6551.4
     try:
         with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -190,25 +206,74 @@ def bench_main(args, metric: str, unit: str) -> int:
         pass
     bytes_rank = max(hi - lo for lo, hi in shard_ranges(V, world)) * esz * (1 + d)
     achieved = bytes_rank / kern_s / 1e9
+    e2e = None
+    if not (getattr(args, "no_e2e", False) or getattr(args, "profile", False)):
+        e2e = _e2e_sharded(args, shard, comm, td, hp, unit)
     if rank == 0:
+        ns = d + d * (d + 1) // 2 + 3
         line = {
             "metric": metric, "value": 1000.0 / ms_step, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if args.storage == "f64" else "f64 (fp32 storage)",
             "data": "synthetic",
             "config": {"workload": f"CAVI sweep, V={V:.0e} genes sharded by octant over {world} GPUs, N={N} "
-                                   f"(d={d}), {args.storage} storage, 1 ncclAllGather of {d + d * (d + 1) // 2 + 2} "
-                                   f"doubles per sweep",
+                                   f"(d={d}), {args.storage} storage, 1 ncclAllGather of {ns} doubles per sweep",
                        "V": V, "N": N, "parallelism": f"dp{world} (gene shards)",
                        "l2": "per-rank stream larger than L2"},
             "gpu_launches": int(nl.value),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "per": "largest rank shard, max over ranks"},
         }
+        if clk is not None:
+            line["clocks"] = clk.summary()
+        if e2e is not None:
+            line["e2e"] = e2e
         print(json.dumps(line), flush=True)
     td.barrier()
     del shard
     return 0
+
+
+def _e2e_sharded(args, shard, comm, td, hp, unit):
+    """vb.vb_fit at N GPUs from host data: per call each rank uploads its pinned shard
+    (H2D inside the timed region), fits with the communicator, reads the state back."""
+    import gc  # noqa: PLC0415
+    import statistics  # noqa: PLC0415
+    import time  # noqa: PLC0415
+
+    import torch  # noqa: PLC0415
+
+    from . import vb  # noqa: PLC0415
+
+    lo, _ = shard_ranges(shard.V_total, comm.world)[comm.rank]
+    V, d = shard.V, shard.dim
+    r, mu, D = _lib.pinned_empty((V,)), _lib.pinned_empty((V,)), _lib.pinned_empty((V, d))
+    r0, mu0, D0 = shard.download()
+    r[:], mu[:], D[:] = r0, mu0, D0
+    del r0, mu0, D0
+    kw = {} if args.e2e_sweeps <= 0 else {"max_iter": args.e2e_sweeps, "rel_tol": 0.0}
+    times, sweeps = [], []
+    for i in range(args.e2e_steps + 1):
+        part = model.Dataset(r=r, mu=mu, D=D, n_networks=shard.n_networks)
+        td.barrier()
+        t0 = time.perf_counter()
+        dd = shard_upload(part, comm, storage=args.storage, V_total=shard.V_total, gene_lo=lo)
+        st, tr = vb.vb_fit(dd, hp, **kw)
+        _ = (st.k0k, st.b_rho, tr.elbo[-1])
+        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+        td.all_reduce(wall, op=td.ReduceOp.MAX)
+        if i:
+            times.append(float(wall[0]))
+            sweeps.append(len(tr))
+        del dd, st, tr, part
+        gc.collect()
+    wall = statistics.median(times)
+    M = int(statistics.median(sweeps))
+    return {"value": M / wall, "unit": unit, "h2d_bytes_per_step": int(8 * shard.V_total * (2 + d)),
+            "d2h_bytes_per_step": int(comm.world * (C.sizeof(_lib.CvState) + 4 * 8 * M)), "sweeps_per_call": M,
+            "call": "per rank: dist.shard_upload(Dataset(host shard, pinned)) + vb.vb_fit(shard, hp)"
+                    + ("  [reference defaults]" if not kw else f", max_iter={M}, rel_tol=0"),
+            "wall_s": wall}
 
 
 __all__ = ["Comm", "Plan", "attach", "bench_main", "init_host_group", "plan", "shard_generate", "shard_ranges",
