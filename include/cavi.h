@@ -223,8 +223,9 @@ void cv_host_free(void* p);
 
 /* ---- measurement hooks (bench.py) ------------------------------------ */
 /* Run `warmup` then `sweeps` CAVI sweeps (ELBO on, no stop rule) from `st`
- * on the dataset's stream; *ms_total = CUDA-event time of the timed sweeps,
- * *ms_kernel = summed CUDA-event time of the fused-pass kernels alone. */
+ * on the dataset's stream; *ms_total = CUDA-event time of the timed sweeps run back to
+ * back as the fit loop runs them; *ms_kernel = summed CUDA-event time of the fused-pass
+ * kernels alone, from a second run of `sweeps` sweeps with events bracketing each pass. */
 int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, int32_t warmup,
                         int32_t sweeps, double* ms_total, double* ms_kernel, int32_t* launches);
 

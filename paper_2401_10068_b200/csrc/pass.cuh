@@ -240,6 +240,8 @@ template <int D>
 __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, Ctl* c, const double* parts, int world) {
   constexpr int NS = n_stats(D);
   __shared__ double tot[NS];
+  ptx::griddep_launch_dependents();  // the next pass may launch and stage its prologue
+  ptx::griddep_wait();               // the pass (or exchange) that produced `parts` is complete
   if (*(volatile const int*)&c->done) return;
   for (int st = threadIdx.x; st < NS; st += 32) {
     double v[kOctants];
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
   double* slots = reinterpret_cast<double*>(smem + G::kOffSlots);  // [kSlots][kWarps][NS]
 
   const Ctl* ctl = a.ctl;
-  if (*(volatile const int*)&ctl->done) return;
+  ptx::griddep_launch_dependents();  // the tail may launch and wait on this grid now
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int q = 0; q < G::kStages; ++q) {
@@ -680,6 +682,9 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
       for (int i = threadIdx.x; i < (G::kCols - D) * G::kColStride; i += blockDim.x) st[i] = (T)0;
     }
   }
+  // everything above is CTA-local: it overlaps the previous kernel under PDL
+  ptx::griddep_wait();
+  if (*(volatile const int*)&ctl->done) return;
   __syncthreads();
   if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 8] = globaltimer_ns();
 

@@ -76,6 +76,14 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// programmatic dependent launch (PDL): let the next kernel in the stream launch now and
+// stage its prologue; wait for the previous kernel's completion (and its memory) before
+// touching anything it wrote.  Both are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // named barrier over a subset of the CTA's warps
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
