@@ -161,17 +161,68 @@ def cpu_reference_sample(V_total, N, target_s=1.0, min_genes=20000):
     return sweep, Vs, sample
 
 
+def _cpu_worker(args):
+    """One worker process: its own gene slice, barrier-started sweeps (see cpu_reference_parallel)."""
+    V_slice, N, steps, barrier, out = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import cavi as ocavi
+    from oracle import philox
+
+    K, Lam, rho = truth(N)
+    r, mu, D = philox.generate(SEED, V_slice, N, K, Lam, rho)
+    hp = ocavi.default_hyper(N)
+    st = ocavi.init(r, mu, D, hp)
+    st = ocavi.step(st, r, mu, D, hp)  # warm-up
+    barrier.wait()
+    for _ in range(steps):
+        nw = ocavi.step(st, r, mu, D, hp)
+        ocavi.elbo(nw, r, mu, D, hp)
+        st = nw
+    barrier.wait()
+    out.put(0)
+
+
+def cpu_reference_parallel(V_total, N, procs=None, steps=2, target_s=2.0):
+    """The reference algorithm on every host core: `procs` processes each sweep a 1/procs
+    slice of a bounded sample (the work of one sweep is a sum over genes), started
+    together; seconds per full-V sweep = wall per sweep x V_total / sample."""
+    import multiprocessing as mp
+
+    procs = procs or os.cpu_count() or 1
+    sweep, Vs1, _ = cpu_reference_sample(V_total, N, target_s=target_s / 2)
+    per_gene = statistics.median([sweep() for _ in range(2)]) / Vs1
+    V_slice = max(1024, int(target_s / per_gene / 1024) * 1024)
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(procs + 1)
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_cpu_worker, args=((V_slice, N, steps, barrier, q),)) for _ in range(procs)]
+    for p_ in ps:
+        p_.start()
+    barrier.wait()
+    t0 = time.perf_counter()
+    barrier.wait()
+    wall = (time.perf_counter() - t0) / steps
+    for p_ in ps:
+        q.get()
+        p_.join()
+    Vs = V_slice * procs
+    sample = (f"{procs} processes x the first {V_slice} genes of the seed-{SEED} N={N} dataset; vb_step+vb_elbo "
+              f"of the reference algorithm (numpy oracle port of tissuemix.vb), {steps} sweeps started together, "
+              f"wall per sweep scaled by {V_total}/{Vs}; single core: {1.0 / (per_gene * V_total):.4g} sweeps/s")
+    return wall * V_total / Vs, procs, sample
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     V = int(args.genes)
-    sweep, Vs, sample = cpu_reference_sample(V, args.networks)
-    for _ in range(max(0, min(args.warmup, 3))):
-        sweep()
-    times = [sweep() for _ in range(args.steps)]
-    per_sweep_full = statistics.median(times) * V / Vs
+    per = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t, cores, sample = cpu_reference_parallel(V, args.networks)
+        per.append(t)
+    per_sweep_full = statistics.median(per)
     value = 1.0 / per_sweep_full
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -179,8 +230,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"CAVI sweep, V={V:.0e} genes, N={args.networks} networks (K={args.networks}), "
                                f"fp64, reference algorithm on host cores (bounded sample)",
-                   "V": V, "N": args.networks, "sample_genes": Vs},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+                   "V": V, "N": args.networks},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -253,11 +304,8 @@ def run_ours(args):
         line["e2e"] = e2e(args, dd, hp)
     del dd
     if not (args.no_cpu or args.profile):
-        sweep, Vs, sample = cpu_reference_sample(V, N, target_s=1.0)
-        sweep()
-        ts = [sweep() for _ in range(8)]
-        cv = 1.0 / (statistics.median(ts) * V / Vs)
-        line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+        t, cores, sample = cpu_reference_parallel(V, N)
+        line["cpu_baseline"] = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     print(json.dumps(line), flush=True)
     return 0
 
