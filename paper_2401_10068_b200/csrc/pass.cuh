@@ -261,11 +261,11 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
 
 typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
 
-// ---------------------------------------------------------------- d >= 4: fp64 tensor cores
+// ------------------------------------------------- d >= CAVI_MMA_MIN_D: fp64 tensor cores
 // mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no fp64 kind).  Per warp and 8 genes:
-//   U = D_8xd A^-1               (s_i = D_i . U_i, t_i = c . D_i, reduced over the 4 lanes of a row)
+//   Y = D_8xd L,  A^-1 = L L^T    (s_i = |Y_i|^2; t_i = c . D_i; see MmaConsumer)
 //   G += (D o gamma)^T D          (2 k-steps of 4 genes; upper tiles only)
-// Fragments (PTX m8n8k4 .f64): A[r=lane/4][q=lane%4], B[q][r], C[r][2q+i].  A^-1 lives in B
+// Fragments (PTX m8n8k4 .f64): A[r=lane/4][q=lane%4], B[q][r], C[r][2q+i].  L lives in B
 // fragments (<= 8 doubles/lane), the d x d accumulator in C fragments (<= 6 doubles/lane), so
 // d = 15 fits in registers; padding columns (>= d) are zero.
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
