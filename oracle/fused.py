@@ -25,8 +25,8 @@ Algebra (reference vb.py:129-198 and vb.py:216-304 rewritten):
 
 Reduction plan (GPU-count invariant, deterministic):
   chunk  = CHUNK_GENES consecutive genes  -> one partial
-  group  = GROUP_CHUNKS consecutive chunks, summed in index order
-  octant = ceil(n_groups/8) consecutive groups, summed in index order
+  group  = GROUP_CHUNKS consecutive chunks, summed by warp_rows_sum (strided lanes + butterfly)
+  octant = ceil(n_groups/8) consecutive groups, summed by warp_rows_sum
   total  = pairwise tree over the 8 octants ((o0+o1)+(o2+o3))+((o4+o5)+(o6+o7))
 A rank of a power-of-two world G<=8 owns 8/G consecutive octants, reduces
 them with its subtree, and the G rank partials are combined by the top of
@@ -133,14 +133,26 @@ def local_stats(x, D, gen: Generator, gene_lo: int, V_total: int):
             raise ValueError("shard boundary does not align with octants")
         acc = np.zeros(ns)
         if lo_l < hi_l:
+            gsums = []
             for g0 in range(lo_l, hi_l, GROUP_CHUNKS * CHUNK_GENES):
-                gacc = np.zeros(ns)
-                for c0 in range(g0, min(g0 + GROUP_CHUNKS * CHUNK_GENES, hi_l), CHUNK_GENES):
-                    seg = terms[c0 - gene_lo: min(c0 + CHUNK_GENES, hi_l) - gene_lo]
-                    gacc = gacc + seg.sum(axis=0)
-                acc = acc + gacc
+                csums = [terms[c0 - gene_lo: min(c0 + CHUNK_GENES, hi_l) - gene_lo].sum(axis=0)
+                         for c0 in range(g0, min(g0 + GROUP_CHUNKS * CHUNK_GENES, hi_l), CHUNK_GENES)]
+                gsums.append(warp_rows_sum(csums))
+            acc = warp_rows_sum(gsums)
         octs.append(acc)
     return octs
+
+
+def warp_rows_sum(rows):
+    """The device's row reduction (pass.cuh warp_sum_rows): lane l adds rows l, l+32, ... in
+    index order from 0.0, then an xor butterfly over 32 lanes; lane 0's value."""
+    ns = rows[0].shape[0]
+    lanes = [np.zeros(ns) for _ in range(32)]
+    for i, r in enumerate(rows):
+        lanes[i % 32] = lanes[i % 32] + r
+    for off in (16, 8, 4, 2, 1):
+        lanes = [lanes[l] + lanes[l ^ off] for l in range(32)]
+    return lanes[0]
 
 
 def combine(rank_partials):

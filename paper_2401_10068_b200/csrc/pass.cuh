@@ -17,8 +17,8 @@
 // larger than L2); 8 consumer warps compute out of shared memory and release
 // stages through "empty" mbarriers.  The thread->gene map inside a chunk is
 // fixed, so each chunk partial is bit-reproducible whatever CTA computes it.
-// Chunk partials -> group (64 chunks, index order, by the CTA that completes
-// the group) -> octants (index order) -> pairwise tree over the octants, by
+// Chunk partials -> group (64 chunks, fixed-order warp reduction, by the CTA that completes
+// the group) -> octants (same) -> pairwise tree over the octants, by
 // the CTA that completes the last group, which then runs the tail
 // (engine.cuh) or, on a multi-GPU shard, publishes its octant subtree.
 #pragma once
@@ -154,36 +154,49 @@ __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const dou
 }
 
 // ---------------------------------------------------------------- deterministic reduction
-// Every level sums its children in index order, so the totals are bit-identical
+// Every level sums its children in a fixed order, so the totals are bit-identical
 // whichever CTA / warp / GPU computed a chunk.  The level that completes a
 // parent (a per-parent arrival counter reaching its child count) computes it;
 // nobody waits for anybody.  Warp-level code: lane l handles statistics
 // l, l+32, ...
 
-// sum_{i<n} src[i*NS + stat] for this lane's stats, index order, loads pipelined
+// sum_{i<n} src[i*NS + stat] in the plan's fixed order: lane l adds rows l, l+32, l+64, ...
+// in index order, then a 32-lane xor butterfly (16, 8, 4, 2, 1); lane 0 writes.  One L2
+// round trip per 32 rows instead of a 16-deep dependent chain per stat column.
 template <int NS>
 __device__ __forceinline__ void warp_sum_rows(const double* src, int64_t n, double* dst, int lane) {
-  for (int st = lane; st < NS; st += 32) {
-    double s = 0.0;
-    for (int64_t i0 = 0; i0 < n; i0 += 16) {
-      double v[16];  // 16 independent loads in flight, then added in index order (+0.0 past the end)
+  constexpr int B = NS < 16 ? NS : 16;  // stats per pass (register budget)
+  for (int s0 = 0; s0 < NS; s0 += B) {
+    double acc[B];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = (i0 + j < n) ? __ldcg(src + (i0 + j) * NS + st) : 0.0;
+    for (int b = 0; b < B; ++b) acc[b] = 0.0;
+#pragma unroll 2
+    for (int64_t i = lane; i < n; i += 32) {
+      const double* row = src + i * NS + s0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) s += v[j];
+      for (int b = 0; b < B; ++b)
+        if (s0 + b < NS) acc[b] += __ldcg(row + b);
     }
-    dst[st] = s;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      double v = acc[b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0 && s0 + b < NS) dst[s0 + b] = v;
+    }
   }
 }
 
 // lane 0 publishes (fence, cumulative over the warp's stores) and counts an arrival
+// (one acq_rel atomic: release publishes the warp's stores, which __syncwarp ordered before
+// lane 0's; acquire makes every other arriver's stores visible to the last one)
 __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned int need, int lane) {
   unsigned int last = 0;
   __syncwarp();
   if (lane == 0) {
-    __threadfence();
-    last = atomicAdd(counter, 1u) == need - 1;
-    if (last) __threadfence();
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+    last = old == need - 1;
   }
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
@@ -200,15 +213,21 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
   if (!warp_arrive_last(a.gcount + grp, (unsigned int)nc, lane)) return;
   // group complete
   if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
-  warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.gpartials + grp * NS, lane);
   const int64_t gg = a.group_lo + grp;  // global group index
   const int o = (int)(gg / a.groups_per_octant);
   const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
   const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
-  if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
-  // octant complete
-  if (lane == 0) a.ocount[o] = 0u;
-  warp_sum_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, a.opartials + o * NS, lane);
+  if (g1 - g0 == 1) {
+    // a one-group octant: its sum over one row is the row itself (the butterfly adds zeros),
+    // so the group completes the octant directly (small V: one arrival level less)
+    warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.opartials + o * NS, lane);
+  } else {
+    warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.gpartials + grp * NS, lane);
+    if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
+    // octant complete
+    if (lane == 0) a.ocount[o] = 0u;
+    warp_sum_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, a.opartials + o * NS, lane);
+  }
   if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
   // every octant this shard owns is complete: pairwise tree over them (empty octants add 0)
   if (lane == 0) *a.odone = 0u;
