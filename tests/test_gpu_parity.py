@@ -183,3 +183,22 @@ def test_batched_fits_mixed_sizes_match_single_fits(eng):
         np.testing.assert_allclose(tr.elbo, t1.elbo, rtol=RTOL, atol=0)
         close(st.k0k, s1.k0k)
         close(st.lam0l_inv, s1.lam0l_inv)
+
+
+def test_batched_result_sequence_semantics(eng):
+    """vb_fit_many returns a lazy sequence: len, indexing (incl. negative), slices, n_iter."""
+    vb, model = eng
+    datasets = []
+    for s in range(5):
+        r, mu, D, _, _ = philox.make_regime(56, 100 + s, 3)
+        datasets.append(model.Dataset(r=r, mu=mu, D=D, n_networks=3))
+    res = vb.vb_fit_many(datasets, model.default_hyperparams(3), max_iter=40)
+    assert len(res) == 5
+    st_last, tr_last = res[-1]
+    st4, tr4 = res[4]
+    assert np.array_equal(st_last.k0k, st4.k0k) and np.array_equal(tr_last.elbo, tr4.elbo)
+    assert [len(t) for _, t in res[1:3]] == [int(n) for n in res.n_iter[1:3]]
+    with pytest.raises(IndexError):
+        res[5]
+    # per-gene fields materialise from the fit's own dataset
+    assert res[2][0].mu_beta.shape == (56, 2)
