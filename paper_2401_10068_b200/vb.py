@@ -287,14 +287,16 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
     np.cumsum(np.fromiter((len(ds.r) for ds in datasets), dtype=np.int64, count=n), out=offsets[1:])
     if offsets[-1] != D.shape[0] or r.shape[0] != D.shape[0]:
         raise ValueError("r, mu and D of a dataset must have the same number of genes")
-    states = (_lib.CvState * n)()
+    # result buffers without a zero fill (1e4 states = 90 MB): the device writes every byte
+    sbuf = np.empty(n * C.sizeof(_lib.CvState), dtype=np.uint8)
+    states = (_lib.CvState * n).from_buffer(sbuf)
     tr = np.empty((n, 4, max_iter))
     hs, keep = _lib.hyper_struct(hp)
     _lib.check(_lib.lib().cv_batched_fit(
         _lib.dptr(r), _lib.dptr(mu), _lib.dptr(D), offsets.ctypes.data_as(C.POINTER(C.c_int64)), n, d,
         C.byref(hs), int(max_iter), float(rel_tol), int(bool(compute_elbo)), float(param_tol),
         _lib.default_device() if device is None else device, states, _lib.dptr(tr)))
-    raw = np.frombuffer(states, dtype=np.uint8).reshape(n, C.sizeof(_lib.CvState))
+    raw = sbuf.reshape(n, C.sizeof(_lib.CvState))
     off = _lib.CvState.n_iter.offset
     n_iter = raw[:, off:off + 4].copy().view(np.int32)[:, 0]
     return FitBatch(datasets, states, tr, n_iter, hp)
