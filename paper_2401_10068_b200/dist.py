@@ -151,6 +151,28 @@ def shard_upload(ds, comm: Comm, storage: str = "f64", V_total: int | None = Non
     return attach(dd, comm)
 
 
+# ----------------------------------------------------------- independent fits (config 4)
+def fit_ranges(n_fits: int, world: int):
+    """Contiguous, balanced split of n_fits independent fits over `world` ranks."""
+    return [(n_fits * r // world, n_fits * (r + 1) // world) for r in range(world)]
+
+
+def fit_many_partitioned(datasets, hp, rank: int | None = None, world: int | None = None, **kw):
+    """vb_fit_many over this rank's share of independent datasets (BASELINE config 4 across
+    GPUs): no collective -- every fit is independent, so each rank fits its slice on its own
+    GPU (LOCAL_RANK) and the caller gathers whatever it needs.  Returns (lo, hi, results)."""
+    from . import vb  # noqa: PLC0415
+
+    r0, w0, local = world_info()
+    rank = r0 if rank is None else rank
+    world = w0 if world is None else world
+    datasets = list(datasets)
+    lo, hi = fit_ranges(len(datasets), world)[rank]
+    if hi == lo:
+        return lo, hi, []
+    return lo, hi, vb.vb_fit_many(datasets[lo:hi], hp, device=kw.pop("device", local), **kw)
+
+
 # ---------------------------------------------------------------------------- bench leg
 def bench_main(args, metric: str, unit: str, clocks_cls=None) -> int:
     """bench.py at N>1: strong scaling of the V-gene sweep over the ranks of torchrun.
@@ -276,5 +298,5 @@ def _e2e_sharded(args, shard, comm, td, hp, unit):
             "wall_s": wall}
 
 
-__all__ = ["Comm", "Plan", "attach", "bench_main", "init_host_group", "plan", "shard_generate", "shard_ranges",
-           "shard_upload", "share_unique_id", "world_info"]
+__all__ = ["Comm", "Plan", "attach", "bench_main", "fit_many_partitioned", "fit_ranges", "init_host_group", "plan",
+           "shard_generate", "shard_ranges", "shard_upload", "share_unique_id", "world_info"]

@@ -77,3 +77,15 @@ def test_two_rank_gloo_exchange_is_bit_identical(tmp_path, world):
         ok = np.load(tmp_path / f"r{rk}.npy")
         assert ok[0], "NCCL unique id did not reach every rank"
         assert ok[1], "rank partials combined by the octant tree differ from the single-rank total"
+
+
+@pytest.mark.parametrize("n,world", [(10000, 8), (7, 8), (1, 2), (12345, 3)])
+def test_fit_ranges_partition_all_fits(n, world):
+    """config 4 across GPUs: every fit on exactly one rank, balanced to within one fit."""
+    from paper_2401_10068_b200 import dist
+
+    spans = dist.fit_ranges(n, world)
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    sizes = [hi - lo for lo, hi in spans]
+    assert max(sizes) - min(sizes) <= 1

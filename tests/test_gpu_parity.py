@@ -202,3 +202,21 @@ def test_batched_result_sequence_semantics(eng):
         res[5]
     # per-gene fields materialise from the fit's own dataset
     assert res[2][0].mu_beta.shape == (56, 2)
+
+
+def test_partitioned_fits_equal_one_batch(eng):
+    """config 4 split over ranks (no collective): the ranks' slices reproduce one batch."""
+    from paper_2401_10068_b200 import dist
+
+    vb, model = eng
+    datasets = []
+    for s in range(11):
+        r, mu, D, _, _ = philox.make_regime(56, 300 + s, 3)
+        datasets.append(model.Dataset(r=r, mu=mu, D=D, n_networks=3))
+    hp = model.default_hyperparams(3)
+    whole = vb.vb_fit_many(datasets, hp, max_iter=60)
+    for rank in range(4):
+        lo, hi, part = dist.fit_many_partitioned(datasets, hp, rank=rank, world=4, device=0, max_iter=60)
+        for i, (st, tr) in enumerate(part):
+            sw, tw = whole[lo + i]
+            assert np.array_equal(tr.elbo, tw.elbo) and np.array_equal(st.k0k, sw.k0k)
