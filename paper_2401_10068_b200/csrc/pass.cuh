@@ -625,6 +625,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_MMA_MIN_D
 #define CAVI_MMA_MIN_D 6  // smallest d served by the DMMA consumer (scalar d=6 spills: 424 vs 704 sweeps/s)
 #endif
+#ifndef CAVI_MMA_SMALL_MAXD
+#define CAVI_MMA_SMALL_MAXD 9  // largest d run at CAVI_MMA_SMALL_BLOCKS CTAs/SM (d=10,11 spill at 3)
+#endif
 #ifndef CAVI_MMA_SMALL_BLOCKS
 #define CAVI_MMA_SMALL_BLOCKS 3  // CTAs per SM for the DMMA consumer at d <= 8
 #endif
@@ -640,7 +643,11 @@ struct Geometry {
   static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
   // small d: per-thread register kernel; larger d: fp64 tensor-core (DMMA) consumer
-  static constexpr int kTile = D <= 1 ? CAVI_TILE_TINY_D : D <= 3 ? CAVI_TILE_SMALL_D : (kMma ? 256 : 512);  // genes/stage
+  static constexpr bool kSmallBlocks = kMma && D <= CAVI_MMA_SMALL_MAXD;
+  // genes per stage; 3 CTAs/SM of the 16-column DMMA stages need half-size tiles
+  static constexpr int kTile = D <= 1 ? CAVI_TILE_TINY_D
+                               : D <= 3 ? CAVI_TILE_SMALL_D
+                               : kMma ? ((kSmallBlocks && D > 8) ? 128 : 256) : 512;
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
@@ -653,7 +660,7 @@ struct Geometry {
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   // the DMMA kernels at d <= 8 (~110 registers) are latency-bound at 2 CTAs/SM: run 3
-  static constexpr int kMinBlocks = (kMma && D <= 8) ? CAVI_MMA_SMALL_BLOCKS : CAVI_MIN_BLOCKS;
+  static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS : CAVI_MIN_BLOCKS;
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
   static constexpr int kDrift = (kSlots - 1) * kTilesPerChunk;
