@@ -1455,6 +1455,7 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   c.cur = *st;
   c.mode = MODE_SWEEP;
   c.rel_tol = 0.0;  // the stop rule never fires: every timed sweep does the full pass
+  if (getenv("CAVI_BENCH_NO_ELBO")) c.compute_elbo = 0;  // diagnostics: the sweep without the bound
   if ((rc = ctl_put(ds, c))) return rc;
   derive_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
   CK(cudaGetLastError());
