@@ -68,3 +68,14 @@ def test_nccl_world1_fit_equals_single_gpu():
     st, tr = vb.vb_fit(shard, hp, max_iter=30)
     assert np.array_equal(tr.elbo, ref_tr.elbo)
     assert np.array_equal(st.lam0l_inv, ref_st.lam0l_inv) and st.b_rho == ref_st.b_rho
+    # EM and the single-step API run through the same exchange (cv_em_fit / cv_step on a shard)
+    from paper_2401_10068_b200 import em
+
+    init = model.ModelParams(K=hp.K0, Lam=hp.Lambda0, rho=1.0)
+    p1, t1 = em.em_fit(model.generate(5, V, N, K, lam, 100.0), init, max_iter=20)
+    p2, t2 = em.em_fit(shard, init, max_iter=20)
+    assert np.array_equal(t1.loglik, t2.loglik) and np.array_equal(p1.K, p2.K)
+    s0 = vb.vb_init(shard, hp)
+    s1 = vb.vb_step(s0, shard, hp)
+    r0 = vb.vb_init(model.generate(5, V, N, K, lam, 100.0), hp)
+    assert s1.b_rho == vb.vb_step(r0, model.generate(5, V, N, K, lam, 100.0), hp).b_rho
