@@ -86,6 +86,7 @@ _SIGS = {
     "cv_nccl_unique_id": (C.c_int32, [C.c_char_p]),
     "cv_comm_create": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "cv_comm_destroy": (None, [C.c_void_p]),
+    "cv_comm_fused": (C.c_int32, [C.c_void_p]),
     "cv_dataset_set_comm": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "cv_dataset_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),

@@ -87,6 +87,11 @@ PassKernel pass_for(int d, int storage) {
 struct cv_comm {
   ncclComm_t nccl = nullptr;
   int rank = 0, world = 1, device = 0;
+  // fused exchange (lsa.cuh): symmetric window of the NCCL device API + sequence counter
+  void* sym = nullptr;
+  ncclWindow_t win = nullptr;
+  unsigned long long* seq = nullptr;
+  int lsa = 0;  // 1: the pass publishes into peers' windows; 0: ncclAllGather
 };
 
 struct cv_dataset {
@@ -213,6 +218,12 @@ int plan_and_alloc(cv_dataset* ds) {
   return CV_OK;
 }
 
+LsaLink lsa_link(const cv_dataset* ds) {
+  LsaLink L{nullptr, nullptr, 1, 0};
+  if (ds->comm && ds->comm->lsa) L = LsaLink{ds->comm->win, ds->comm->seq, ds->comm->world, ds->comm->rank};
+  return L;
+}
+
 PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   PassArgs a;
   a.x = ds->x;
@@ -236,6 +247,7 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.ctl = ds->ctl;
   a.hyp = ds->hyp;
   a.rank_out = rank_out;
+  a.lsa = lsa_link(ds);
   a.cta_trace = ds->cta_trace;
   a.l2_keep = ds->device_bytes < (size_t)64 << 20;
   return a;
@@ -263,9 +275,70 @@ cudaLaunchConfig_t pdl_config(unsigned grid, unsigned threads, size_t smem, cuda
   return cfg;
 }
 
+void lsa_teardown(cv_comm* c) {
+  if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+  if (c->sym) ncclMemFree(c->sym);
+  if (c->seq) cudaFree(c->seq);
+  c->win = nullptr;
+  c->sym = nullptr;
+  c->seq = nullptr;
+  c->lsa = 0;
+}
+
+// Collective (every rank calls it from cv_comm_create): map a symmetric window, run the
+// bounded self-test exchange, and agree (allreduce min) on whether the fused path is on.
+// Every collective call is preceded by an agreement, so a local failure on any rank can
+// never leave the others blocked: every rank then keeps the ncclAllGather exchange.
+int agree(cv_comm* c, int* dflag, int ok) {
+  int all = 0;
+  if (cudaMemcpy(dflag, &ok, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) ok = 0;
+  if (ncclAllReduce(dflag, dflag, 1, ncclInt32, ncclMin, c->nccl, 0) != ncclSuccess) return 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+  if (cudaMemcpy(&all, dflag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return all;
+}
+
+void lsa_setup(cv_comm* c) {
+  int* dflag = nullptr;
+  if (cudaMalloc(&dflag, 2 * sizeof(int)) != cudaSuccess) return;  // (no collective issued yet)
+  int ok = getenv("CAVI_NO_LSA") ? 0 : 1;
+  if (ok && ncclTeamLsa(c->nccl).nRanks != c->world) ok = 0;  // one NVLink domain only
+  if (ok && ncclMemAlloc(&c->sym, kLsaWindowBytes) != ncclSuccess) ok = 0;
+  if (ok && cudaMemset(c->sym, 0, kLsaWindowBytes) != cudaSuccess) ok = 0;
+  if (ok && cudaMalloc(&c->seq, sizeof(unsigned long long)) != cudaSuccess) ok = 0;
+  if (ok && cudaMemset(c->seq, 0, sizeof(unsigned long long)) != cudaSuccess) ok = 0;
+  ok = agree(c, dflag, ok);
+  if (ok && ncclCommWindowRegister(c->nccl, c->sym, kLsaWindowBytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
+    c->win = nullptr;
+    ok = 0;
+  }
+  ok = agree(c, dflag, ok);
+  if (ok) {
+    cudaMemset(dflag + 1, 0, sizeof(int));
+    lsa_selftest_kernel<<<1, 32>>>(LsaLink{c->win, c->seq, c->world, c->rank}, 1ull, dflag + 1);
+    int got = 0;
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(&got, dflag + 1, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+      got = 0;
+    const unsigned long long one = 1;  // the self-test used sequence 1
+    if (got && cudaMemcpy(c->seq, &one, sizeof one, cudaMemcpyHostToDevice) != cudaSuccess) got = 0;
+    ok = agree(c, dflag, got);
+  }
+  cudaFree(dflag);
+  if (ok == 1) {
+    c->lsa = 1;
+    return;
+  }
+  lsa_teardown(c);
+}
+
 int launch_pass_only(cv_dataset* ds) {
   if (ds->n_chunks == 0) {  // a rank that holds no genes contributes exact zeros
-    CK(cudaMemsetAsync(rank_slot(ds), 0, sizeof(double) * n_stats(ds->d), ds->stream));
+    if (ds->comm && ds->comm->lsa) {
+      lsa_publish_zeros_kernel<<<1, 32, 0, ds->stream>>>(lsa_link(ds), n_stats(ds->d), &ds->ctl->done);
+      CK(cudaGetLastError());
+    } else {
+      CK(cudaMemsetAsync(rank_slot(ds), 0, sizeof(double) * n_stats(ds->d), ds->stream));
+    }
     return CV_OK;
   }
   cudaLaunchConfig_t cfg = pdl_config(ds->grid, ds->pass.threads, ds->pass.smem, ds->stream);
@@ -275,7 +348,7 @@ int launch_pass_only(cv_dataset* ds) {
 
 // multi-GPU exchange: every rank receives every rank's octant-subtree partial (88 B at d=3)
 int launch_exchange(cv_dataset* ds) {
-  if (!ds->comm) return CV_OK;
+  if (!ds->comm || ds->comm->lsa) return CV_OK;  // fused: the pass already published into every peer
   const int ns = n_stats(ds->d);
   ncclResult_t r = ncclAllGather(ds->gathered + (size_t)ds->comm->rank * ns, ds->gathered, ns, ncclDouble,
                                  ds->comm->nccl, ds->stream);
@@ -289,7 +362,7 @@ int launch_tail_only(cv_dataset* ds) {
   const int world = ds->comm ? ds->comm->world : 1;
   cudaLaunchConfig_t cfg = pdl_config(1, 32, 0, ds->stream);
   const double* parts = ds->comm ? ds->gathered : ds->tot;
-  CK(cudaLaunchKernelEx(&cfg, ds->pass.tail, (const Hyp*)ds->hyp, ds->ctl, parts, world));
+  CK(cudaLaunchKernelEx(&cfg, ds->pass.tail, (const Hyp*)ds->hyp, ds->ctl, parts, world, lsa_link(ds)));
   return CV_OK;
 }
 
@@ -459,12 +532,16 @@ int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t d
     delete c;
     return fail(CV_ERR_CUDA, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  lsa_setup(c);
   *out = c;
   return CV_OK;
 }
 
+int32_t cv_comm_fused(cv_comm* c) { return c ? c->lsa : 0; }
+
 void cv_comm_destroy(cv_comm* c) {
   if (!c) return;
+  lsa_teardown(c);
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
 }

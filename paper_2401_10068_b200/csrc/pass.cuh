@@ -24,6 +24,7 @@
 #pragma once
 
 #include "engine.cuh"
+#include "lsa.cuh"
 #include "ptx.cuh"
 
 namespace cavi {
@@ -50,6 +51,7 @@ struct PassArgs {
   Ctl* ctl;
   const Hyp* hyp;
   double* rank_out;        // [ns] totals of this shard (its octant subtree), read by the tail kernel
+  LsaLink lsa;             // multi-GPU: publish the shard totals into every peer (lsa.win != null)
   unsigned long long* cta_trace;  // optional [grid][8] globaltimer stamps (diagnostics)
 };
 
@@ -61,7 +63,7 @@ struct PassKernel {
   PassFn fn;
   int threads;
   int smem;  // dynamic shared memory bytes
-  void (*tail)(const Hyp*, Ctl*, const double*, int);
+  void (*tail)(const Hyp*, Ctl*, const double*, int, LsaLink);
   void (*batched)(BatchArgs);
   void (*wishart_seg)(WishartArgs);
   void (*wishart_fin)(WishartArgs, const double*, const double*, double, uint64_t, double*, double*);
@@ -235,7 +237,7 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
     a.cta_trace[blockIdx.x * 8 + 4] = t_entry;
     a.cta_trace[blockIdx.x * 8 + 5] = globaltimer_ns();
   }
-  for (int st = lane; st < NS; st += 32) {
+  auto total = [&](int st) {
     double v[kOctants];
 #pragma unroll
     for (int q = 0; q < kOctants; ++q) v[q] = 0.0;
@@ -246,7 +248,12 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
     }
     for (int w = 1; w < a.oct_hi - a.oct_lo; w *= 2)
       for (int q = a.oct_lo; q + w < a.oct_hi; q += 2 * w) v[q] = v[q] + v[q + w];
-    a.rank_out[st] = v[a.oct_lo];
+    return v[a.oct_lo];
+  };
+  if (a.lsa.win) {  // fused exchange: straight into every peer's window over NVLink
+    lsa_publish(a.lsa, *a.lsa.seq + 1, NS, total, lane);
+  } else {
+    for (int st = lane; st < NS; st += 32) a.rank_out[st] = total(st);
   }
   (void)s_tot;
   if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
@@ -256,18 +263,39 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
 // dependent scalar chain and must not spill): pairwise tree over the `world` shard
 // totals (1 on a single GPU; the NCCL-gathered rank partials otherwise), then tail_t.
 template <int D>
-__global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, Ctl* c, const double* parts, int world) {
+__global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, Ctl* c, const double* parts, int world,
+                                                     LsaLink lsa) {
   constexpr int NS = n_stats(D);
   __shared__ double tot[NS];
   ptx::griddep_launch_dependents();  // the next pass may launch and stage its prologue
   ptx::griddep_wait();               // the pass (or exchange) that produced `parts` is complete
   if (*(volatile const int*)&c->done) return;
-  for (int st = threadIdx.x; st < NS; st += 32) {
-    double v[kOctants];
-    for (int r = 0; r < world; ++r) v[r] = __ldcg(parts + r * NS + st);
-    for (int w = 1; w < world; w *= 2)
-      for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
-    tot[st] = v[0];
+  if (lsa.win) {  // fused exchange: every rank's partial arrives in this rank's window
+    const uint64_t s = *lsa.seq + 1;
+    if (!lsa_wait(lsa, s, threadIdx.x, 1ll << 33)) {  // ~4 s: a peer stalled -> error, not a hang
+      if (threadIdx.x == 0) {
+        c->status = CV_ERR_CUDA;
+        c->done = 1;
+      }
+      return;
+    }
+    for (int st = threadIdx.x; st < NS; st += 32) {
+      double v[kOctants];
+      for (int r = 0; r < world; ++r) v[r] = lsa_read(lsa, s, r, st);
+      for (int w = 1; w < world; w *= 2)
+        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
+      tot[st] = v[0];
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) *lsa.seq = s;
+  } else {
+    for (int st = threadIdx.x; st < NS; st += 32) {
+      double v[kOctants];
+      for (int r = 0; r < world; ++r) v[r] = __ldcg(parts + r * NS + st);
+      for (int w = 1; w < world; w *= 2)
+        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
+      tot[st] = v[0];
+    }
   }
   __syncwarp();
   if (threadIdx.x == 0) {
@@ -278,7 +306,7 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
   }
 }
 
-typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int);
+typedef void (*TailFn)(const Hyp*, Ctl*, const double*, int, LsaLink);
 
 // ------------------------------------------------- d >= CAVI_MMA_MIN_D: fp64 tensor cores
 // mma.sync.m8n8k4.f64 (DMMA; tcgen05 has no fp64 kind).  Per warp and 8 genes:

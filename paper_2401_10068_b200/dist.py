@@ -102,6 +102,12 @@ class Comm:
     def handle(self):
         return self._h
 
+    @property
+    def fused(self) -> bool:
+        """True when the per-sweep exchange is fused into the pass (NVLink stores into the
+        peers' NCCL symmetric windows); False: one ncclAllGather per sweep."""
+        return bool(_lib.lib().cv_comm_fused(self._h))
+
     @classmethod
     def bootstrap(cls, device: int | None = None, td=None) -> "Comm":
         td = td or init_host_group()
@@ -239,7 +245,9 @@ def bench_main(args, metric: str, unit: str, clocks_cls=None) -> int:
             "vs_baseline": None, "dtype": "f64" if args.storage == "f64" else "f64 (fp32 storage)",
             "data": "synthetic",
             "config": {"workload": f"CAVI sweep, V={V:.0e} genes sharded by octant over {world} GPUs, N={N} "
-                                   f"(d={d}), {args.storage} storage, 1 ncclAllGather of {ns} doubles per sweep",
+                                   f"(d={d}), {args.storage} storage, per-sweep exchange of {ns} doubles: "
+                                   + ("fused into the pass (NVLink stores into NCCL symmetric windows)"
+                                      if comm.fused else "one ncclAllGather"),
                        "V": V, "N": N, "parallelism": f"dp{world} (gene shards)",
                        "l2": "per-rank stream larger than L2"},
             "gpu_launches": int(nl.value),

@@ -79,3 +79,30 @@ def test_nccl_world1_fit_equals_single_gpu():
     s1 = vb.vb_step(s0, shard, hp)
     r0 = vb.vb_init(model.generate(5, V, N, K, lam, 100.0), hp)
     assert s1.b_rho == vb.vb_step(r0, model.generate(5, V, N, K, lam, 100.0), hp).b_rho
+
+
+def test_fused_exchange_is_active_and_exact():
+    """The fused exchange (pass -> peers' symmetric windows) passed its self-test at
+    cv_comm_create, and a fit through it equals the single-GPU fit (world 1: the window is
+    this GPU's own; the flags / parity / sequence logic runs exactly as with 8 ranks)."""
+    import torch.distributed as td
+
+    from paper_2401_10068_b200 import dist, model, vb
+
+    if not td.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        td.init_process_group("gloo", rank=0, world_size=1)
+    comm = dist.Comm.bootstrap(device=0, td=td)
+    assert comm.fused
+    V, N = 600_000, 3
+    K, lam = np.array([0.1, 0.3]), np.linalg.inv(model.REFERENCE_LAMBDA_INV)
+    hp = model.default_hyperparams(N)
+    ref_st, ref_tr = vb.vb_fit(model.generate(8, V, N, K, lam, 100.0), hp, max_iter=80)
+    shard = dist.shard_generate(8, V, N, K, lam, 100.0, comm)
+    for _ in range(2):  # several fits: the sequence counter and parities keep advancing
+        st, tr = vb.vb_fit(shard, hp, max_iter=80)
+        assert np.array_equal(tr.elbo, ref_tr.elbo) and st.b_rho == ref_st.b_rho
