@@ -146,7 +146,7 @@ int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t d
 void cv_comm_destroy(cv_comm* c);
 /* 1 when the exchange is fused into the pass (peer stores into NCCL symmetric windows over
  * NVLink, checked by a collective self-test at cv_comm_create); 0: ncclAllGather per sweep.
- * CAVI_NO_LSA=1 forces the NCCL path. */
+ * CAVI_NO_LSA=1 forces the NCCL path; a world of one uses neither (CAVI_LSA_WORLD1=1: fused). */
 int32_t cv_comm_fused(cv_comm* c);
 int32_t cv_dataset_set_comm(cv_dataset* ds, cv_comm* comm);
 /* Mark a shard as rank `rank` of `world` without a communicator (single-GPU

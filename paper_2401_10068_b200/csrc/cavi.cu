@@ -301,7 +301,10 @@ int agree(cv_comm* c, int* dflag, int ok) {
 void lsa_setup(cv_comm* c) {
   int* dflag = nullptr;
   if (cudaMalloc(&dflag, 2 * sizeof(int)) != cudaSuccess) return;  // (no collective issued yet)
+  // one GPU needs no exchange at all (its partial is read in place); CAVI_LSA_WORLD1=1 runs
+  // the fused protocol against its own window anyway (tests)
   int ok = getenv("CAVI_NO_LSA") ? 0 : 1;
+  if (c->world == 1 && !getenv("CAVI_LSA_WORLD1")) ok = 0;
   if (ok && ncclTeamLsa(c->nccl).nRanks != c->world) ok = 0;  // one NVLink domain only
   if (ok && ncclMemAlloc(&c->sym, kLsaWindowBytes) != ncclSuccess) ok = 0;
   if (ok && cudaMemset(c->sym, 0, kLsaWindowBytes) != cudaSuccess) ok = 0;

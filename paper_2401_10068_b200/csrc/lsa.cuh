@@ -60,20 +60,21 @@ __device__ __forceinline__ void lsa_publish(const LsaLink& L, uint64_t s, int ns
     for (int p = 0; p < L.world; ++p)
       static_cast<double*>(ncclGetLsaPointer(L.win, lsa_data_off(par, L.rank), p))[st] = v;
   }
-  __threadfence_system();  // every lane's remote stores before any flag
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // every lane's remote stores before any flag
   __syncwarp();
   if (lane < L.world)
     st_release_sys(static_cast<uint64_t*>(ncclGetLsaPointer(L.win, lsa_flag_off(par, L.rank), lane)), s);
 }
 
-// One warp: wait until every rank published sequence s (bounded), then each lane reads the
-// per-rank partials of its statistics from this rank's window.  Returns false on timeout.
+// One warp: wait until every rank published sequence s (bounded).  Every lane acquires
+// every flag itself (and sees it reach s) before it reads any data the flags guard.
+// Returns false on timeout (uniformly across the warp).
 __device__ __forceinline__ bool lsa_wait(const LsaLink& L, uint64_t s, int lane, long long max_cycles) {
   const int par = (int)(s & 1);
   bool ok = true;
-  if (lane < L.world) {
-    const uint64_t* f = static_cast<const uint64_t*>(ncclGetLocalPointer(L.win, lsa_flag_off(par, lane)));
-    const long long t0 = clock64();
+  const long long t0 = clock64();
+  for (int r = 0; r < L.world && ok; ++r) {
+    const uint64_t* f = static_cast<const uint64_t*>(ncclGetLocalPointer(L.win, lsa_flag_off(par, r)));
     while (ld_acquire_sys(f) < s) {
       if (clock64() - t0 > max_cycles) {
         ok = false;
@@ -81,12 +82,7 @@ __device__ __forceinline__ bool lsa_wait(const LsaLink& L, uint64_t s, int lane,
       }
     }
   }
-  ok = __all_sync(0xffffffffu, ok);
-  // every lane acquires every flag itself before reading the data it guards
-  if (ok)
-    for (int r = 0; r < L.world; ++r)
-      (void)ld_acquire_sys(static_cast<const uint64_t*>(ncclGetLocalPointer(L.win, lsa_flag_off(par, r))));
-  return ok;
+  return __all_sync(0xffffffffu, ok);
 }
 
 __device__ __forceinline__ double lsa_read(const LsaLink& L, uint64_t s, int rank, int st) {
