@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(kBatchThreads) batched_fit_kernel(BatchArgs a)
       lg.mul(gene<D>(k, x, Dv, acc));
     }
     acc[stat_Ld(D)] = lg.log_value();
-    tail_t<D>(h, c, acc);
+    double Tm[D * D], hv[D];
+    pass_products_t<D>(c.pass.Ainv, acc, Tm, hv);
+    tail_t<D>(h, c, acc, Tm, hv);
     if (c.done) break;
   }
 }

@@ -1590,6 +1590,12 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   for (auto& e : evs) cudaEventDestroy(e);
   if (launches) *launches = 2 * sweeps;  // fused pass + tail kernel per sweep
   if ((rc = ctl_get(ds))) return rc;
+  if (getenv("CAVI_TAIL_PROF_PRINT")) {
+    const unsigned long long* p = ds->h_ctl->prof;
+    fprintf(stderr, "tail cycles: combine %lld loads %lld update %lld elbo %lld bookkeeping %lld stores %lld\n",
+            (long long)(p[6] - p[0]), (long long)(p[1] - p[6]), (long long)(p[2] - p[1]), (long long)(p[3] - p[2]),
+            (long long)(p[4] - p[3]), (long long)(p[5] - p[4]));
+  }
   if (ds->h_ctl->status != CV_OK) return state_status(ds->h_ctl->cur);
   return CV_OK;
 }

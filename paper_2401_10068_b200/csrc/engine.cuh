@@ -97,7 +97,14 @@ struct Ctl {
   double* tr_dlam;
   double* tr_k;  // EM: K per iteration [tr_cap][d]
   int tr_cap;
+  unsigned long long prof[8];  // CAVI_TAIL_PROF builds: clock64 stamps of the last tail
 };
+
+#ifdef CAVI_TAIL_PROF
+#define TAIL_PROF(c, i) ((c).prof[i] = clock64())
+#else
+#define TAIL_PROF(c, i) ((void)0)
+#endif
 
 // ------------------------------------------------------------------ special functions
 static __device__ inline double digamma_pos(double x) {
@@ -331,18 +338,10 @@ struct GenT {
 // vb_elbo (reference vb.py:216-304) of the state (a, b, k0k, S = lam0l_inv^-1,
 // ln|lam0l_inv|), whose per-gene moments come from generator `gen`, from the
 // pass statistics of that generator.
+// Tm = Ainv G Ainv (full), hv = Ainv g from a pass's statistics [g | G upper | ...]
 template <int D>
-__device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, const double* k0k, const double* S,
-                                         double ln_det_l, const GenT<D>& gen, const double* stats, int* status) {
-  if (!h.proper_q) {
-    *status = CV_ERR_IMPROPER;
-    return qnan();
-  }
-  constexpr int NS = n_stats(D);
-  const double V = h.V, nu = h.nu, qv = h.qv;
-  const double R = stats[stat_R(D)];
-  const double Ld = stats[stat_Ld(D)];
-  double G[D * D], Ai[D * D];
+__device__ __forceinline__ void pass_products_t(const double* Ai, const double* stats, double* Tm, double* hv) {
+  double G[D * D], AG[D * D];
   {
     int p = D;
 #pragma unroll
@@ -355,26 +354,12 @@ __device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, c
       }
   }
 #pragma unroll
-  for (int i = 0; i < D * D; ++i) Ai[i] = gen.Ainv[i];
-  const double ln_s = -ln_det_l;
-  const double dga = (a == h.a_fit) ? h.dg_afit : (a == h.a0 ? h.dg_a0 : digamma_pos(a));
-  const double lga = (a == h.a_fit) ? h.lg_afit : (a == h.a0 ? h.lg_a0 : lgamma(a));
-  const double e_rho = a / b;
-  const double lnb = log(b);
-  const double e_lnrho = dga - lnb;
-  const double e_lnlam = h.sum_dg_nu + D * kLn2 + ln_s;
-  // hv = Ainv g, dlt = k0k - c
-  double hv[D], dlt[D];
-#pragma unroll
   for (int i = 0; i < D; ++i) {
     double t = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
     hv[i] = t;
-    dlt[i] = k0k[i] - gen.c[i];
   }
-  // scatter = V Ainv + Ainv G Ainv - dlt h^T - h dlt^T + V dlt dlt^T ; tr(S scatter)
-  double AG[D * D];
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -384,15 +369,48 @@ __device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, c
       for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
       AG[i * D + j] = t;
     }
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) t += AG[i * D + k] * Ai[k * D + j];
+      Tm[i * D + j] = t;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, const double* k0k, const double* S,
+                                         double ln_det_l, const GenT<D>& gen, const double* stats, const double* Tm,
+                                         const double* hv, int* status) {
+  // Tm = Ainv G Ainv and hv = Ainv g of this pass (shared with the (K, Lambda) update)
+  if (!h.proper_q) {
+    *status = CV_ERR_IMPROPER;
+    return qnan();
+  }
+  const double V = h.V, nu = h.nu, qv = h.qv;
+  const double R = stats[stat_R(D)];
+  const double Ld = stats[stat_Ld(D)];
+  const double* Ai = gen.Ainv;
+  const double ln_s = -ln_det_l;
+  const double dga = (a == h.a_fit) ? h.dg_afit : (a == h.a0 ? h.dg_a0 : digamma_pos(a));
+  const double lga = (a == h.a_fit) ? h.lg_afit : (a == h.a0 ? h.lg_a0 : lgamma(a));
+  const double e_rho = a / b;
+  const double lnb = log(b);
+  const double e_lnrho = dga - lnb;
+  const double e_lnlam = h.sum_dg_nu + D * kLn2 + ln_s;
+  double dlt[D];  // k0k - c
+#pragma unroll
+  for (int i = 0; i < D; ++i) dlt[i] = k0k[i] - gen.c[i];
+  // scatter = V Ainv + Ainv G Ainv - dlt h^T - h dlt^T + V dlt dlt^T ; tr(S scatter)
   double tr1 = 0.0, quad = 0.0, tr0 = 0.0;
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      double T = 0.0;
-#pragma unroll
-      for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
-      const double sc = V * Ai[i * D + j] + T - dlt[i] * hv[j] - hv[i] * dlt[j] + V * dlt[i] * dlt[j];
+      const double sc = V * Ai[i * D + j] + ((const volatile double*)Tm)[i * D + j] - dlt[i] * hv[j] - hv[i] * dlt[j] +
+                        V * dlt[i] * dlt[j];
       const double sij = S[i * D + j];
       tr1 += sij * sc;
       quad += (k0k[i] - h.K0[i]) * sij * (k0k[j] - h.K0[j]);
@@ -453,7 +471,10 @@ static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
 // a single thread runs it at the end of every sweep, so its dependent global round trips
 // (not its flops) are what the sweep pays for.
 template <int D>
-__device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
+__device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats, const double* Tm,
+                                       const double* hv) {
+  // Tm / hv: Ainv G Ainv and Ainv g of this pass (pass_products_t; the warp computes them in
+  // tail_kernel, a batched thread for itself)
   constexpr int NS = n_stats(D);
   // ---- loads (independent, issued back to back)
   HypT<D> h;
@@ -479,11 +500,12 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
 #pragma unroll
   for (int i = 0; i < D * D; ++i) l_old[i] = s.lam0l_inv[i];
 
+  TAIL_PROF(c, 1);
   if (mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
     double S[D * D], ld;
     int es = CV_ERR_NUMERIC;
     double e = qnan();
-    if (spd_inv_logdet_t<D>(l_old, S, &ld)) e = elbo_t<D>(h, a_old, b_old, k_old, S, ld_old, gen, st, &es);
+    if (spd_inv_logdet_t<D>(l_old, S, &ld)) e = elbo_t<D>(h, a_old, b_old, k_old, S, ld_old, gen, st, Tm, hv, &es);
     s.elbo = e;
     s.elbo_status = es;
     return;
@@ -513,49 +535,22 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
     // (K, Lambda) block, centred (vb.py:172-183):
     //   dlt = (Ainv g + q0 (K0 - c)) / qv ; k0k = c + dlt
     //   lam0l_inv = L0inv + V Ainv + Ainv G Ainv + q0 (K0-c)(K0-c)^T - qv dlt dlt^T
-    double G[D * D];
-    {
-      int p = D;
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int k = j; k < D; ++k) {
-          G[j * D + k] = st[p];
-          G[k * D + j] = st[p];
-          ++p;
-        }
-    }
     const double* Ai = gen.Ainv;
     double k0c[D], dlt[D];
     const double rqv = 1.0 / h.qv;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      double t = 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) t += Ai[i * D + j] * st[j];
       k0c[i] = h.K0[i] - gen.c[i];
-      dlt[i] = (t + h.q0 * k0c[i]) * rqv;
+      dlt[i] = (hv[i] + h.q0 * k0c[i]) * rqv;
       k_new[i] = gen.c[i] + dlt[i];
     }
-    double AG[D * D];
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        double t = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
-        AG[i * D + j] = t;
-      }
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = i; j < D; ++j) {
-        double T = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
         const double v =
-            h.L0inv[i * D + j] + h.V * Ai[i * D + j] + T + h.q0 * k0c[i] * k0c[j] - h.qv * dlt[i] * dlt[j];
+            h.L0inv[i * D + j] + h.V * Ai[i * D + j] + ((const volatile double*)Tm)[i * D + j] + h.q0 * k0c[i] * k0c[j] -
+            h.qv * dlt[i] * dlt[j];
         L[i * D + j] = v;
         L[j * D + i] = v;
       }
@@ -564,9 +559,12 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
     b = pend_b;
     e_rho = gen.e_rho;
   }
+  TAIL_PROF(c, 2);
   double elbo = qnan();
   int elbo_status = CV_OK;
-  if (status == CV_OK && (compute_elbo || mode == MODE_INIT)) elbo = elbo_t<D>(h, a, b, k_new, S, ld, gen, st, &elbo_status);
+  if (status == CV_OK && (compute_elbo || mode == MODE_INIT))
+    elbo = elbo_t<D>(h, a, b, k_new, S, ld, gen, st, Tm, hv, &elbo_status);
+  TAIL_PROF(c, 3);
   double elamk[D];
 #pragma unroll
   for (int i = 0; i < D; ++i) {
@@ -603,6 +601,7 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
     done = 1;
   }
 
+  TAIL_PROF(c, 4);
   // ---- stores
   s.status = status;
   s.d = D;
@@ -658,6 +657,7 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
     c.pend_b = nb;
     c.pass.e_rho = h.a_fit / nb;
   }
+  TAIL_PROF(c, 5);
 }
 
 // ------------------------------------------------------------------ EM (reference em.py)

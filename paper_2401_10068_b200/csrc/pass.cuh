@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
   __shared__ double tot[NS];
   ptx::griddep_launch_dependents();  // the next pass may launch and stage its prologue
   ptx::griddep_wait();               // the pass (or exchange) that produced `parts` is complete
+  if (threadIdx.x == 0) TAIL_PROF(*c, 0);
   if (*(volatile const int*)&c->done) return;
   if (lsa.win) {  // fused exchange: every rank's partial arrives in this rank's window
     const uint64_t s = *lsa.seq + 1;
@@ -298,11 +299,41 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
     }
   }
   __syncwarp();
+  // Ainv G Ainv and Ainv g (the O(d^3) part of the tail) across the warp: lane i owns row i
+  __shared__ double sA[D * D], sAG[D * D], sT[D * D], shv[D];
+  const int mode = c->mode;
+  if (mode != MODE_EM) {
+    for (int i = threadIdx.x; i < D * D; i += 32) sA[i] = c->pass.Ainv[i];
+    __syncwarp();
+    const int i = threadIdx.x;
+    if (i < D) {
+      double t = 0.0;
+      for (int j = 0; j < D; ++j) t += sA[i * D + j] * tot[j];
+      shv[i] = t;
+      for (int j = 0; j < D; ++j) {
+        double u = 0.0;
+        for (int k = 0; k < D; ++k) {
+          const int lo = k < j ? k : j, hi = k < j ? j : k;
+          u += sA[i * D + k] * tot[D + lo * D - lo * (lo - 1) / 2 + (hi - lo)];
+        }
+        sAG[i * D + j] = u;
+      }
+    }
+    __syncwarp();
+    if (i < D)
+      for (int j = 0; j < D; ++j) {
+        double u = 0.0;
+        for (int k = 0; k < D; ++k) u += sAG[i * D + k] * sA[k * D + j];
+        sT[i * D + j] = u;
+      }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) TAIL_PROF(*c, 6);
   if (threadIdx.x == 0) {
-    if (c->mode == MODE_EM)
+    if (mode == MODE_EM)
       em_tail_t<D>(*h, *c, tot);
     else
-      tail_t<D>(*h, *c, tot);
+      tail_t<D>(*h, *c, tot, sT, shv);
   }
 }
 
