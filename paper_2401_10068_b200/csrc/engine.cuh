@@ -294,12 +294,35 @@ static __device__ __noinline__ void hyp_setup(Hyp& h) {
 
 // Register/stack copy of the hyperparameters a d-specialised tail needs, loaded in
 // one burst of independent loads (the tail is latency-bound: one thread, end of sweep).
+// A fixed-size read-only block: a register copy, or a pointer to the global original.
+template <int N, bool Reg>
+struct Mat {
+  double v[N];
+  __device__ __forceinline__ void load(const double* __restrict__ p) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = p[i];
+  }
+  __device__ __forceinline__ double operator[](int i) const { return v[i]; }
+  __device__ __forceinline__ operator const double*() const { return v; }
+};
+template <int N>
+struct Mat<N, false> {
+  const double* v;
+  __device__ __forceinline__ void load(const double* p) { v = p; }
+  __device__ __forceinline__ double operator[](int i) const { return v[i]; }
+  __device__ __forceinline__ operator const double*() const { return v; }
+};
+
 template <int D>
 struct HypT {
+  // d x d blocks: registers for small d; for d > 8 (4 x 225 doubles would spill the whole
+  // tail to local memory) they stay in the L1-cached global structs and are read in place
+  static constexpr bool kReg = D <= 8;
   int n0, has_zprior, proper_q;
   double a0, b0, q0, V, nu, qv, lnL0, zprior, a_fit, dg_afit, lg_afit, dg_a0, lg_a0, sum_dg_nu, mgl_nu;
   double ln_nu, ln_q0, ln_qv, ln_b0;
-  double K0[D], L0[D * D], L0inv[D * D];
+  double K0[D];
+  Mat<D * D, kReg> L0, L0inv;
   __device__ __forceinline__ void load(const Hyp& __restrict__ h) {
     n0 = h.n0;
     has_zprior = h.has_zprior;
@@ -309,26 +332,23 @@ struct HypT {
     sum_dg_nu = h.sum_dg_nu; mgl_nu = h.mgl_nu; ln_nu = h.ln_nu; ln_q0 = h.ln_q0; ln_qv = h.ln_qv; ln_b0 = h.ln_b0;
 #pragma unroll
     for (int i = 0; i < D; ++i) K0[i] = h.K0[i];
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) {
-      L0[i] = h.L0[i];
-      L0inv[i] = h.L0inv[i];
-    }
+    L0.load(h.L0);
+    L0inv.load(h.L0inv);
   }
 };
 
-// the generator a pass streamed against, in registers
+// the generator a pass streamed against, in registers (d x d blocks in place for d > 8)
 template <int D>
 struct GenT {
-  double c[D], A[D * D], Ainv[D * D], lnA, e_rho;
+  static constexpr bool kReg = D <= 8;
+  double c[D];
+  Mat<D * D, kReg> A, Ainv;
+  double lnA, e_rho;
   __device__ __forceinline__ void load(const Gen& __restrict__ g) {
 #pragma unroll
     for (int i = 0; i < D; ++i) c[i] = g.c[i];
-#pragma unroll
-    for (int i = 0; i < D * D; ++i) {
-      A[i] = g.A[i];
-      Ainv[i] = g.Ainv[i];
-    }
+    A.load(g.A);
+    Ainv.load(g.Ainv);
     lnA = g.lnA;
     e_rho = g.e_rho;
   }
@@ -493,12 +513,12 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
   double st[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) st[i] = stats[i];
-  double k_old[D], l_old[D * D];
+  double k_old[D];
+  Mat<D * D, (D <= 8)> l_old;  // read in place for d > 8 (the stores below come after its last use)
   const double e_rho_old = s.e_rho, a_old = s.a_rho, b_old = s.b_rho, ld_old = s.ln_det_lam0l_inv;
 #pragma unroll
   for (int i = 0; i < D; ++i) k_old[i] = s.k0k[i];
-#pragma unroll
-  for (int i = 0; i < D * D; ++i) l_old[i] = s.lam0l_inv[i];
+  l_old.load(s.lam0l_inv);
 
   TAIL_PROF(c, 1);
   if (mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
