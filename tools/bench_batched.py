@@ -22,13 +22,14 @@ def main():
     p.add_argument("--networks", type=int, default=3)
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
-    from oracle import philox  # input generation only (the reference's Philox stream)
     from paper_2401_10068_b200 import model, vb
 
     hp = model.default_hyperparams(a.networks)
     for nf in a.fits:
         nf = int(nf)
-        r, mu, D, _, _ = philox.make_regime(nf * a.genes, 56, a.networks)
+        dd = model.regime(nf * a.genes, 56, a.networks)  # the reference test regime, generated on the GPU
+        r, mu, D = dd.download()
+        dd.close()
         dss = [model.Dataset(r=r[i * a.genes:(i + 1) * a.genes], mu=mu[i * a.genes:(i + 1) * a.genes],
                              D=D[i * a.genes:(i + 1) * a.genes], n_networks=a.networks) for i in range(nf)]
         vb.vb_fit_many(dss[: min(nf, 64)], hp)  # warm-up
