@@ -273,19 +273,21 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
   if (*(volatile const int*)&c->done) return;
   if (lsa.win) {  // fused exchange: every rank's partial arrives in this rank's window
     const uint64_t s = *lsa.seq + 1;
-    if (!lsa_wait(lsa, s, threadIdx.x, 1ll << 33)) {  // ~4 s: a peer stalled -> error, not a hang
+    const long long deadline = clock64() + (1ll << 33);  // ~4 s: a peer stalled -> error, not a hang
+    bool ok = true;
+    for (int st = threadIdx.x; st < NS; st += 32) {
+      double v[kOctants];
+      for (int r = 0; r < world; ++r) v[r] = lsa_take(lsa, s, r, st, deadline, &ok);
+      for (int w = 1; w < world; w *= 2)
+        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
+      tot[st] = v[0];
+    }
+    if (!__all_sync(0xffffffffu, ok)) {
       if (threadIdx.x == 0) {
         c->status = CV_ERR_CUDA;
         c->done = 1;
       }
       return;
-    }
-    for (int st = threadIdx.x; st < NS; st += 32) {
-      double v[kOctants];
-      for (int r = 0; r < world; ++r) v[r] = lsa_read(lsa, s, r, st);
-      for (int w = 1; w < world; w *= 2)
-        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
-      tot[st] = v[0];
     }
     __syncwarp();
     if (threadIdx.x == 0) *lsa.seq = s;

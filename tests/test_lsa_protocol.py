@@ -1,6 +1,8 @@
 """The fused multi-GPU exchange protocol (csrc/lsa.cuh), modelled on the CPU: W ranks as
 threads with random delays run pass -> publish(s) / tail -> wait(s) -> read for many
-sweeps over the same two-parity window layout.  Asserts that every tail reads exactly
+sweeps over the same two-parity window layout (the device tags every word with its
+sequence number, LL-style; the model keeps one tag per rank slot, which is the same
+validity rule).  Asserts that every tail reads exactly
 sweep s's partials from every rank (the double-buffer argument in lsa.cuh) and that the
 sequence numbers stay in lock step.  (The device code itself is exercised by the GPU
 tests; a world of >1 GPU is not available in this environment.)"""
