@@ -1423,8 +1423,13 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
   const int np = d * (d + 1) / 2;
   const int64_t nu = (int64_t)n0 + V;
   const double qv = q0 + (double)V;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, 4000000 / std::max<int64_t>(nu * d, 1)));
+  // the reference's RNG request size (vb.py:378) fixes the stream layout; a launch covers as
+  // many whole requests as the segment partials' memory (<= 256 MB) allows
+  const int64_t rchunk = std::max<int64_t>(1, std::min<int64_t>(n, 4000000 / std::max<int64_t>(nu * d, 1)));
+  const uint64_t chunk_blocks = (uint64_t)((rchunk * nu * d + 1) / 2) + (uint64_t)((rchunk * d + 1) / 2);
   const int64_t n_seg = (nu + kPostSegRows - 1) / kPostSegRows;
+  const int64_t per_launch = std::max<int64_t>(1, ((int64_t)32 << 20) / std::max<int64_t>(n_seg * np * rchunk, 1));
+  const int64_t chunk = std::min<int64_t>(n, per_launch * rchunk);
   double *dLam, *dR, *dk0k, *lam_d, *k_d, *seg, *val, *raw, *rho_d;
   char* flags;
   int64_t* nsel;
@@ -1456,6 +1461,8 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
     wa.nu = nu;
     wa.n_draws = m;
     wa.block0 = block;
+    wa.rchunk = rchunk;
+    wa.chunk_blocks = chunk_blocks;
     wa.n_seg = n_seg;
     wa.seg_out = seg;
     for (int64_t k0 = 0; k0 < m; k0 += max_m) {
@@ -1464,12 +1471,14 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
       pk.wishart_seg<<<dim3((unsigned)n_seg, gy), kPostThreads, 0, st>>>(wa);
     }
     CK(cudaGetLastError());
-    const uint64_t block_k = block + (uint64_t)((m * nu * d + 1) / 2);
     wa.k_base = 0;
-    pk.wishart_fin<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(wa, dR, dk0k, qv, block_k, lam_d + done * d * d,
+    pk.wishart_fin<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(wa, dR, dk0k, qv, 0, lam_d + done * d * d,
                                                                 k_d + done * d);
     CK(cudaGetLastError());
-    block = block_k + (uint64_t)((m * d + 1) / 2);
+    for (int64_t c0 = 0; c0 < m; c0 += rchunk) {  // the stream each reference request consumed
+      const int64_t mc = std::min<int64_t>(rchunk, m - c0);
+      block += (uint64_t)((mc * nu * d + 1) / 2) + (uint64_t)((mc * d + 1) / 2);
+    }
     done += m;
   }
   // rho ~ Gamma(a_rho, b_rho) by the reference's rejection rounds (samplers.py:220-261)

@@ -35,12 +35,29 @@ struct WishartArgs {
   uint64_t seed, stream_id;
   int d;
   int64_t nu;
-  int64_t n_draws;       // draws in this chunk
-  int64_t k_base;        // first draw (within the chunk) of this launch
-  uint64_t block0;       // first block of this chunk's u = normals(m nu d)
+  int64_t n_draws;       // draws in this launch (whole reference chunks but possibly the last)
+  int64_t k_base;        // first draw (within the launch) of this grid slice
+  uint64_t block0;       // first block of the launch's first reference chunk
+  int64_t rchunk;        // the reference's draws per RNG request (vb.py:378)
+  uint64_t chunk_blocks; // blocks a full chunk consumes: u = normals(rchunk nu d), then normals(rchunk d)
   int64_t n_seg;         // segments per draw
   double* seg_out;       // [n_draws][n_seg][d(d+1)/2]
 };
+
+// Stream position of draw k of a launch: its reference chunk c, index j inside it, the
+// chunk's first block and its draw count.
+struct DrawPos {
+  int64_t j, m;
+  uint64_t base;
+};
+__device__ __forceinline__ DrawPos draw_pos(const WishartArgs& a, int64_t k) {
+  const int64_t c = k / a.rchunk;
+  DrawPos p;
+  p.j = k - c * a.rchunk;
+  p.m = a.n_draws - c * a.rchunk < a.rchunk ? a.n_draws - c * a.rchunk : a.rchunk;
+  p.base = a.block0 + (uint64_t)c * a.chunk_blocks;
+  return p;
+}
 
 __device__ __forceinline__ uint4 philox_block_s(uint64_t seed, uint64_t sid, uint64_t blk) {
   return philox4x32_10(make_uint4((unsigned)blk, (unsigned)(blk >> 32), (unsigned)sid, (unsigned)(sid >> 32)),
@@ -58,8 +75,10 @@ __global__ void __launch_bounds__(kPostThreads) wishart_segment_kernel(WishartAr
 #pragma unroll
   for (int p = 0; p < NP; ++p) acc[p] = 0.0;
   if (row_lo < a.nu) {
-    // elements of this thread: [e0, e1) of the chunk's normals
-    const uint64_t e0 = ((uint64_t)k * a.nu + row_lo) * D, e1 = ((uint64_t)k * a.nu + row_hi) * D;
+    // elements of this thread: [e0, e1) of its reference chunk's normals
+    const DrawPos dp = draw_pos(a, k);
+    const uint64_t e0 = ((uint64_t)dp.j * a.nu + row_lo) * D, e1 = ((uint64_t)dp.j * a.nu + row_hi) * D;
+    const uint64_t base = dp.base;
     double row[D];
     int j = 0;
     auto push = [&](double v) {
@@ -78,11 +97,11 @@ __global__ void __launch_bounds__(kPostThreads) wishart_segment_kernel(WishartAr
     };
     uint64_t e = e0;
     if (e & 1) {  // first element is the second half of a block
-      push(block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1))).y);
+      push(block_normals(philox_block_s(a.seed, a.stream_id, base + (e >> 1))).y);
       ++e;
     }
     for (; e < e1; e += 2) {
-      const double2 nn = block_normals(philox_block_s(a.seed, a.stream_id, a.block0 + (e >> 1)));
+      const double2 nn = block_normals(philox_block_s(a.seed, a.stream_id, base + (e >> 1)));
       push(nn.x);
       if (e + 1 < e1) push(nn.y);
     }
@@ -108,7 +127,7 @@ __global__ void __launch_bounds__(kPostThreads) wishart_segment_kernel(WishartAr
 // one thread per draw: W = sum of segments (index order); Lambda = R W R^T;
 // K = k0k + chol(inv(qv Lambda)) u_k with u_k = normals(m d) of the chunk
 template <int D>
-__global__ void wishart_finish_kernel(WishartArgs a, const double* R, const double* k0k, double qv, uint64_t block_k,
+__global__ void wishart_finish_kernel(WishartArgs a, const double* R, const double* k0k, double qv, uint64_t,
                                       double* lam_out, double* k_out) {
   constexpr int NP = D * (D + 1) / 2;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -154,8 +173,10 @@ __global__ void wishart_finish_kernel(WishartArgs a, const double* R, const doub
     return;
   }
   double uk[D];
+  const DrawPos dp = draw_pos(a, k);
+  const uint64_t block_k = dp.base + (uint64_t)((dp.m * a.nu * D + 1) / 2);  // after the chunk's u
   for (int j = 0; j < D; ++j) {
-    const uint64_t e = (uint64_t)k * D + j;
+    const uint64_t e = (uint64_t)dp.j * D + j;
     const double2 nn = block_normals(philox_block_s(a.seed, a.stream_id, block_k + (e >> 1)));
     uk[j] = (e & 1) ? nn.y : nn.x;
   }
