@@ -1,26 +1,26 @@
-// pass.cuh -- the fused CAVI E-pass: one streaming read of the measurement
-// stream per sweep, per-gene rank-1 beta block in registers, deterministic
-// hierarchical reduction, and the sweep tail in the last CTA.
+// pass.cuh -- the fused CAVI E-pass: one streaming read of the measurement stream per
+// sweep, per-gene rank-1 beta block, deterministic hierarchical reduction; plus the
+// one-warp tail kernel that turns the pass statistics into the next state.
 //
 // Restates, per gene i (reference vb.py:146-170 + vb.py:114-126 + vb.py:233-258):
 //   Lambda_beta_i = A + e_rho D_i D_i^T, mu_beta_i = Lambda_beta_i^-1 (A c + e_rho x_i D_i)
 // via Sherman-Morrison:  s = D^T A^-1 D, t = D^T c, den = 1 + e_rho s,
 //   w = e_rho (x - t)/den,  gamma = w^2 - e_rho/den,  resid = (x - t - s w)^2 + s/den
-// accumulating  g += w D,  G += gamma D D^T,  R += resid,  Ld += ln den.
+// accumulating  g += w D,  G += gamma D D^T,  R += resid,  Q += w (x - t),  Ld += ln den.
 //
 // HBM layout (SoA, padded to whole chunks with zero genes, which contribute
 // exactly 0 to every statistic):  x[Vp] then D column j at D + j*Vp.
 //
-// Kernel (sm_100a, persistent, one CTA per SM): a producer warp streams the
-// CTA's chunks tile by tile into a ring of shared-memory stages with TMA bulk
-// copies (cp.async.bulk + mbarrier complete_tx, L2 evict-first for streams
-// larger than L2); 8 consumer warps compute out of shared memory and release
-// stages through "empty" mbarriers.  The thread->gene map inside a chunk is
-// fixed, so each chunk partial is bit-reproducible whatever CTA computes it.
-// Chunk partials -> group (64 chunks, fixed-order warp reduction, by the CTA that completes
-// the group) -> octants (same) -> pairwise tree over the octants, by
-// the CTA that completes the last group, which then runs the tail
-// (engine.cuh) or, on a multi-GPU shard, publishes its octant subtree.
+// Kernel (sm_100a, persistent, 2-3 CTAs per SM): a producer warp streams the CTA's
+// chunks (dynamic tickets) tile by tile into a ring of shared-memory stages with TMA
+// bulk copies (cp.async.bulk + mbarrier complete_tx, L2 evict-first for streams larger
+// than L2); 4 consumer warps compute out of shared memory (d <= 5: one gene per thread
+// in registers; d >= 6: fp64 tensor cores, MmaConsumer) and release stages through
+// "empty" mbarriers.  The thread->gene map inside a chunk is fixed, so each chunk
+// partial is bit-reproducible whatever CTA computes it.  Chunk partials -> group (64
+// chunks) -> octants -> pairwise tree over the octants, each level by whichever warp
+// completes it (fixed-order sums); the last one writes the shard totals, or on a
+// multi-GPU shard stores them into every peer's window (lsa.cuh).
 #pragma once
 
 #include "engine.cuh"
