@@ -354,6 +354,9 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifndef CAVI_SEMI_Y_MAXD
+#define CAVI_SEMI_Y_MAXD 13  // d > CAVI_HYBRID_MAX_D: trailing Y columns in scalar up to this d (14, 15 spill)
+#endif
 #ifndef CAVI_HYBRID_MAX_D
 #define CAVI_HYBRID_MAX_D 11  // largest d with the scalar trailing block (d = 12 spills: slower)
 #endif
@@ -377,6 +380,11 @@ struct MmaConsumer {
   static constexpr bool kSemi = D > 8 && !kHyb;
   static constexpr int RT = (kHyb || kSemi) ? D - 8 : 0;  // trailing dimensions done in scalar
   static constexpr int MTG = kSemi ? 1 : NT;              // G row tiles on the tensor cores
+  // d > CAVI_HYBRID_MAX_D too: the trailing Y columns (k >= 8) as per-gene scalar FMAs with
+  // the trailing block of L in registers, instead of the Y tiles of column block 1
+  static constexpr bool kSemiY = kSemi && D <= CAVI_SEMI_Y_MAXD;
+  static constexpr int RY = (kHyb || kSemiY) ? D - 8 : 0;  // trailing Y columns done in scalar
+  static constexpr int NTU = RY > 0 ? 1 : NT;               // Y tiles on the tensor cores
   static constexpr int KS = (D + 3) / 4;      // k-steps of Y = D L (rows >= D are zero)
   static constexpr int NS = n_stats(D);
   // s = D^T A^-1 D = |L^T D|^2 with A^-1 = L L^T: Y = D L is block lower-triangular, so the
@@ -393,8 +401,8 @@ struct MmaConsumer {
   LogAcc lg;
   // hybrid extras (RX > 0): trailing block of L, c; per-lane accumulators of the trailing
   // G columns (ge: rows < 8, gl: rows >= 8, packed upper) and of g
-  static constexpr int RXa = RX > 0 ? RX : 1, RTa = RT > 0 ? RT : 1;
-  double lx[RXa * (RXa + 1) / 2], cx[RXa];
+  static constexpr int RXa = RX > 0 ? RX : 1, RTa = RT > 0 ? RT : 1, RYa = RY > 0 ? RY : 1;
+  double lx[RYa * (RYa + 1) / 2], cx[RYa];
   double ge[8][RXa], gl[RTa * (RTa + 1) / 2], gx[RTa];
 
   // L = chol(A^-1), warp-cooperative: lane i holds row i (right-looking, one column per
@@ -441,12 +449,12 @@ struct MmaConsumer {
         const int col = nt * 8 + 2 * q + i;
         cc[nt][i] = col < D ? g.c[col] : 0.0;
       }
-    if constexpr (kHyb) {
+    if constexpr (RY > 0) {
 #pragma unroll
-      for (int k = 0; k < RX; ++k) {
+      for (int k = 0; k < RY; ++k) {
         cx[k] = g.c[8 + k];
 #pragma unroll
-        for (int j = k; j < RX; ++j) lx[j * (j + 1) / 2 + k] = __shfl_sync(0xffffffffu, l[8 + k], 8 + j);
+        for (int j = k; j < RY; ++j) lx[j * (j + 1) / 2 + k] = __shfl_sync(0xffffffffu, l[8 + k], 8 + j);
       }
     }
     erho = g.e_rho;
@@ -494,19 +502,19 @@ struct MmaConsumer {
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
         const int g0 = gb + g * 8;
-        double u[NT][2];
+        double u[NTU][2];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) u[nt][0] = u[nt][1] = 0.0;
+        for (int nt = 0; nt < NTU; ++nt) u[nt][0] = u[nt][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const double av = (double)Dc[(ks * 4 + q) * CS + g0 + r];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
+          for (int nt = 0; nt < NTU; ++nt)
             if (live(ks, nt)) dmma(u[nt], av, bfr[nt][ks]);
         }
         double s_ = 0.0, t_ = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NTU; ++nt)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int col = nt * 8 + 2 * q + i;
@@ -542,12 +550,12 @@ struct MmaConsumer {
 #pragma unroll
         for (int j = kHyb ? 0 : 8; j < D; ++j) dx[j] = (double)Dc[j * CS + own];
       }
-      if constexpr (kHyb) {  // trailing Y columns and t terms of the own gene
+      if constexpr (RY > 0) {  // trailing Y columns and t terms of the own gene
 #pragma unroll
-        for (int k = 0; k < RX; ++k) {
+        for (int k = 0; k < RY; ++k) {
           double y = 0.0;
 #pragma unroll
-          for (int j = k; j < RX; ++j) y = fma(dx[8 + j], lx[j * (j + 1) / 2 + k], y);
+          for (int j = k; j < RY; ++j) y = fma(dx[8 + j], lx[j * (j + 1) / 2 + k], y);
           sv = fma(y, y, sv);
           tv = fma(cx[k], dx[8 + k], tv);
         }
