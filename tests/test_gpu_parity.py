@@ -220,3 +220,28 @@ def test_partitioned_fits_equal_one_batch(eng):
         for i, (st, tr) in enumerate(part):
             sw, tw = whole[lo + i]
             assert np.array_equal(tr.elbo, tw.elbo) and np.array_equal(st.k0k, sw.k0k)
+
+
+def test_dimension_limit_is_a_value_error(eng):
+    """N <= 16 networks (d <= 15) on the device path; beyond that a clean ValueError."""
+    vb, model = eng
+    rng = np.random.default_rng(0)
+    V, N = 50, 17
+    D = rng.integers(0, 2, (V, N - 1)).astype(float)
+    ds = model.Dataset(r=rng.standard_normal(V), mu=np.zeros(V), D=D, n_networks=N)
+    hp = model.HyperParams(a0=0.5, b0=0.5, q0=0.001, n0=1, K0=np.full(N - 1, 1 / 3), Lambda0=100.0 * np.eye(N - 1))
+    with pytest.raises(ValueError):
+        vb.vb_fit(ds, hp, max_iter=3)
+
+
+def test_em_on_fp32_storage_within_1e4(eng):
+    """EM through the optional fp32 stream agrees with the fp64 stream to 1e-4."""
+    from paper_2401_10068_b200 import em
+
+    vb, model = eng
+    hp = model.default_hyperparams(4)
+    init = model.ModelParams(K=hp.K0, Lam=hp.Lambda0, rho=1.0)
+    p64, t64 = em.em_fit(model.regime(200_000, 9, 4), init, max_iter=30, rel_tol=0.0)
+    p32, t32 = em.em_fit(model.regime(200_000, 9, 4, storage="f32"), init, max_iter=30, rel_tol=0.0)
+    np.testing.assert_allclose(t32.loglik, t64.loglik, rtol=1e-4)
+    np.testing.assert_allclose(p32.K, p64.K, rtol=1e-4)
