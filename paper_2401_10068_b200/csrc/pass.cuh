@@ -354,6 +354,12 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifndef CAVI_TINY_BLOCKS
+#define CAVI_TINY_BLOCKS 4  // CTAs per SM at d = 1 (~90 registers; N=2: 3450 -> 3960 sweeps/s)
+#endif
+#ifndef CAVI_D2_BLOCKS
+#define CAVI_D2_BLOCKS 3  // CTAs per SM at d = 2 (118 registers; N=3: 2536 -> 2829 sweeps/s)
+#endif
 #ifndef CAVI_SEMI_Y_MAXD
 #define CAVI_SEMI_Y_MAXD 13  // d > CAVI_HYBRID_MAX_D: trailing Y columns in scalar up to this d (14, 15 spill)
 #endif
@@ -682,7 +688,7 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #define CAVI_TILE_SMALL_D 1024  // genes per stage for d <= 3
 #endif
 #ifndef CAVI_TILE_TINY_D
-#define CAVI_TILE_TINY_D 2048  // genes per stage for d = 1 (N=2: 3116 -> 3291 sweeps/s)
+#define CAVI_TILE_TINY_D 1024  // genes per stage for d = 1
 #endif
 #ifndef CAVI_SMEM_BUDGET
 #define CAVI_SMEM_BUDGET 100000
@@ -729,7 +735,10 @@ struct Geometry {
   static constexpr int kNS = n_stats(D);
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   // the DMMA kernels at d <= 8 (~110 registers) are latency-bound at 2 CTAs/SM: run 3
-  static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS : CAVI_MIN_BLOCKS;
+  static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS
+                                   : D <= 1     ? CAVI_TINY_BLOCKS
+                                   : D == 2     ? CAVI_D2_BLOCKS
+                                                : CAVI_MIN_BLOCKS;
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
   static constexpr int kDrift = (kSlots - 1) * kTilesPerChunk;
