@@ -360,6 +360,12 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 #ifndef CAVI_D2_BLOCKS
 #define CAVI_D2_BLOCKS 3  // CTAs per SM at d = 2 (118 registers; N=3: 2536 -> 2829 sweeps/s)
 #endif
+#ifndef CAVI_D4_BLOCKS
+#define CAVI_D4_BLOCKS 3  // CTAs per SM at d = 4 (128 registers; N=5: 1507 -> 1564 sweeps/s; d = 5 spills at 3)
+#endif
+#ifndef CAVI_TILE_MID
+#define CAVI_TILE_MID 512  // genes per stage of the register path at d = 4, 5
+#endif
 #ifndef CAVI_SEMI_Y_MAXD
 #define CAVI_SEMI_Y_MAXD 13  // d > CAVI_HYBRID_MAX_D: trailing Y columns in scalar up to this d (14, 15 spill)
 #endif
@@ -722,7 +728,7 @@ struct Geometry {
   // genes per stage; 3 CTAs/SM of the 16-column DMMA stages need half-size tiles
   static constexpr int kTile = D <= 1 ? CAVI_TILE_TINY_D
                                : D <= 3 ? CAVI_TILE_SMALL_D
-                               : kMma ? ((kSmallBlocks && D > 8) ? 128 : 256) : 512;
+                               : kMma ? ((kSmallBlocks && D > 8) ? 128 : 256) : CAVI_TILE_MID;
   static constexpr int kTilesPerChunk = kChunk / kTile;
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
@@ -738,6 +744,7 @@ struct Geometry {
   static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS
                                    : D <= 1     ? CAVI_TINY_BLOCKS
                                    : D == 2     ? CAVI_D2_BLOCKS
+                                   : D == 4     ? CAVI_D4_BLOCKS
                                                 : CAVI_MIN_BLOCKS;
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
