@@ -149,6 +149,35 @@ cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s, int device) {
   }
   return cudaMallocAsync(p, std::max<size_t>(bytes, 16), s);
 }
+// Scratch owned by one C-ABI call: every early return (CK) still frees it and the stream.
+struct CallScratch {
+  std::vector<void*> dev;
+  std::vector<void*> pool;  // stream-ordered pool allocations
+  cudaStream_t st = nullptr;
+  ~CallScratch() {
+    for (void* q : pool) cudaFreeAsync(q, st);
+    if (st) cudaStreamSynchronize(st);
+    for (void* q : dev) cudaFree(q);
+    if (st) cudaStreamDestroy(st);
+  }
+  template <typename P>
+  cudaError_t alloc(P** out, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+    if (e == cudaSuccess) dev.push_back(q);
+    *out = (P*)q;
+    return e;
+  }
+  template <typename P>
+  cudaError_t palloc(P** out, size_t bytes, int device) {
+    void* q = nullptr;
+    const cudaError_t e = pool_alloc(&q, bytes ? bytes : 16, st, device);
+    if (e == cudaSuccess) pool.push_back(q);
+    *out = (P*)q;
+    return e;
+  }
+};
+
 #define PALLOC(ptr, bytes) CK(pool_alloc((void**)&(ptr), (bytes), ds->stream, ds->device))
 
 int plan_and_alloc(cv_dataset* ds) {
@@ -1350,21 +1379,22 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
     if (!std::isfinite(D[i])) return fail(CV_ERR_NONFINITE, "non-finite values in A");
   PassKernel pk = pass_for(d, CV_STORE_F64);
   CK(cudaSetDevice(device));
-  cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CallScratch sc;
+  CK(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+  cudaStream_t st = sc.st;
   double *dr, *dmu, *dD, *dtr;
   int64_t* doff;
   Hyp *base, *hyps;
   Ctl* ctls;
   // stream-ordered pool allocations: repeated batches reuse the HBM (release threshold max)
-  CK(pool_alloc((void**)&dr, sizeof(double) * G, st, device));
-  CK(pool_alloc((void**)&dmu, sizeof(double) * G, st, device));
-  CK(pool_alloc((void**)&dD, sizeof(double) * G * d, st, device));
-  CK(pool_alloc((void**)&doff, sizeof(int64_t) * (n_fits + 1), st, device));
-  CK(pool_alloc((void**)&base, sizeof(Hyp), st, device));
-  CK(pool_alloc((void**)&hyps, sizeof(Hyp) * n_fits, st, device));
-  CK(pool_alloc((void**)&ctls, sizeof(Ctl) * n_fits, st, device));
-  CK(pool_alloc((void**)&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, st, device));
+  CK(sc.palloc(&dr, sizeof(double) * G, device));
+  CK(sc.palloc(&dmu, sizeof(double) * G, device));
+  CK(sc.palloc(&dD, sizeof(double) * G * d, device));
+  CK(sc.palloc(&doff, sizeof(int64_t) * (n_fits + 1), device));
+  CK(sc.palloc(&base, sizeof(Hyp), device));
+  CK(sc.palloc(&hyps, sizeof(Hyp) * n_fits, device));
+  CK(sc.palloc(&ctls, sizeof(Ctl) * n_fits, device));
+  CK(sc.palloc(&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, device));
   CK(cudaMemcpyAsync(dr, r, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * G * d, cudaMemcpyHostToDevice, st));
@@ -1397,10 +1427,7 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
   std::vector<int> status(n_fits);
   CK(cudaMemcpy2DAsync(status.data(), sizeof(int), &ctls[0].status, sizeof(Ctl), sizeof(int), n_fits,
                        cudaMemcpyDeviceToHost, st));
-  for (void* p : {(void*)dr, (void*)dmu, (void*)dD, (void*)doff, (void*)base, (void*)hyps, (void*)ctls, (void*)dtr})
-    cudaFreeAsync(p, st);
   CK(cudaStreamSynchronize(st));
-  cudaStreamDestroy(st);
   for (int64_t f = 0; f < n_fits; ++f) {
     if (status[f] == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "fit %lld: Q(Lambda) is improper; dataset too small", (long long)f);
     if (status[f] != CV_OK) return fail(status[f], "fit %lld failed with status %d", (long long)f, status[f]);
@@ -1418,35 +1445,39 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
   if (!(a_rho > 0 && b_rho > 0)) return fail(CV_ERR_ARG, "gamma parameters must be positive, got a=%g, b=%g", a_rho, b_rho);
   PassKernel pk = pass_for(d, CV_STORE_F64);
   CK(cudaSetDevice(device));
-  cudaStream_t st;
-  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CallScratch sc;
+  CK(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
+  cudaStream_t st = sc.st;
   const int np = d * (d + 1) / 2;
   const int64_t nu = (int64_t)n0 + V;
   const double qv = q0 + (double)V;
   // the reference's RNG request size (vb.py:378) fixes the stream layout; a launch covers as
-  // many whole requests as the segment partials' memory (<= 256 MB) allows
+  // many whole requests as the bounds below allow
   const int64_t rchunk = std::max<int64_t>(1, std::min<int64_t>(n, 4000000 / std::max<int64_t>(nu * d, 1)));
   const uint64_t chunk_blocks = (uint64_t)((rchunk * nu * d + 1) / 2) + (uint64_t)((rchunk * d + 1) / 2);
   const int64_t n_seg = (nu + kPostSegRows - 1) / kPostSegRows;
-  const int64_t per_launch = std::max<int64_t>(1, ((int64_t)32 << 20) / std::max<int64_t>(n_seg * np * rchunk, 1));
+  // (<= 4M doubles of segment partials and <= 256k CTAs per launch: enough to fill the GPU)
+  const int64_t per_launch = std::max<int64_t>(
+      1, std::min<int64_t>(((int64_t)4 << 20) / std::max<int64_t>(n_seg * np * rchunk, 1),
+                           ((int64_t)256 << 10) / std::max<int64_t>(n_seg * rchunk, 1)));
   const int64_t chunk = std::min<int64_t>(n, per_launch * rchunk);
   double *dLam, *dR, *dk0k, *lam_d, *k_d, *seg, *val, *raw, *rho_d;
   char* flags;
   int64_t* nsel;
   int* prep;
-  CK(cudaMalloc(&dLam, sizeof(double) * 2 * kMaxD2));
+  CK(sc.alloc(&dLam, sizeof(double) * 2 * kMaxD2));
   dR = dLam + kMaxD2;
-  CK(cudaMalloc(&dk0k, sizeof(double) * kMaxD));
-  CK(cudaMalloc(&lam_d, sizeof(double) * n * d * d));
-  CK(cudaMalloc(&k_d, sizeof(double) * n * d));
+  CK(sc.alloc(&dk0k, sizeof(double) * kMaxD));
+  CK(sc.alloc(&lam_d, sizeof(double) * n * d * d));
+  CK(sc.alloc(&k_d, sizeof(double) * n * d));
   const int64_t max_m = std::min<int64_t>(chunk, 65535);
-  CK(cudaMalloc(&seg, sizeof(double) * std::max<int64_t>(chunk, 1) * n_seg * np));
-  CK(cudaMalloc(&val, sizeof(double) * n));
-  CK(cudaMalloc(&raw, sizeof(double) * n));
-  CK(cudaMalloc(&rho_d, sizeof(double) * n));
-  CK(cudaMalloc(&flags, n));
-  CK(cudaMalloc(&nsel, sizeof(int64_t)));
-  CK(cudaMalloc(&prep, sizeof(int)));
+  CK(sc.alloc(&seg, sizeof(double) * std::max<int64_t>(chunk, 1) * n_seg * np));
+  CK(sc.alloc(&val, sizeof(double) * n));
+  CK(sc.alloc(&raw, sizeof(double) * n));
+  CK(sc.alloc(&rho_d, sizeof(double) * n));
+  CK(sc.alloc(&flags, n));
+  CK(sc.alloc(&nsel, sizeof(int64_t)));
+  CK(sc.alloc(&prep, sizeof(int)));
   CK(cudaMemcpyAsync(dLam, lam0l_inv, sizeof(double) * d * d, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dk0k, k0k, sizeof(double) * d, cudaMemcpyHostToDevice, st));
   // R = chol(inv(lam0l_inv)) in the reference's operation order (vb.py:375-376)
@@ -1488,7 +1519,7 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   CK(cub::DeviceSelect::Flagged(nullptr, tmp_bytes, val, flags, raw, nsel, (int64_t)n, st));
-  CK(cudaMalloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
+  CK(sc.alloc(&tmp, std::max<size_t>(tmp_bytes, 16)));
   int64_t filled = 0;
   while (filled < n) {
     const int64_t todo = n - filled;
@@ -1514,10 +1545,6 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
   int pst = 0;
   CK(cudaMemcpyAsync(&pst, prep, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  for (void* p : {(void*)dLam, (void*)dk0k, (void*)lam_d, (void*)k_d, (void*)seg, (void*)val, (void*)raw,
-                  (void*)rho_d, (void*)flags, (void*)nsel, (void*)prep, tmp})
-    cudaFree(p);
-  cudaStreamDestroy(st);
   if (pst != CV_OK) return fail(CV_ERR_NUMERIC, "non-positive pivot in the Q(Lambda) scale");
   *block_end = block;
   return CV_OK;
