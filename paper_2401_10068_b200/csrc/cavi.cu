@@ -1258,14 +1258,14 @@ static int em_setup(cv_dataset* ds, const double* K, const double* Lam, double r
   c.tr_dlam = ds->trace + 3 * (size_t)ds->trace_cap;
   c.tr_k = ds->trace + 4 * (size_t)ds->trace_cap;
   if ((rc = ctl_put(ds, c))) return rc;
-  double* dp = nullptr;  // theta_0 staged through the hyper block's workspace
-  CK(cudaMalloc(&dp, sizeof(double) * (kMaxD + kMaxD2)));
+  double* dp = nullptr;  // theta_0 staged through a scratch buffer
+  CallScratch sc;
+  CK(sc.alloc(&dp, sizeof(double) * (kMaxD + kMaxD2)));
   CK(cudaMemcpyAsync(dp, K, sizeof(double) * ds->d, cudaMemcpyHostToDevice, ds->stream));
   CK(cudaMemcpyAsync(dp + kMaxD, Lam, sizeof(double) * ds->d * ds->d, cudaMemcpyHostToDevice, ds->stream));
   em_init_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl, dp, dp + kMaxD, rho);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ds->stream));
-  CK(cudaFree(dp));
   return CV_OK;
 }
 
@@ -1343,8 +1343,9 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
   double* outs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double* hosts[5] = {mu_beta, lam_beta, e_bbt, sigma, resid};
   const size_t per[5] = {(size_t)d, (size_t)d * d, (size_t)d * d, (size_t)d * d, 1};
+  CallScratch sc;  // frees the outputs on every return (the dataset's stream is not owned)
   for (int q = 0; q < 5; ++q)
-    if (hosts[q]) CK(cudaMalloc(&outs[q], sizeof(double) * n * per[q]));
+    if (hosts[q]) CK(sc.alloc(&outs[q], sizeof(double) * n * per[q]));
   const int tb = 128;
   const unsigned blocks = (unsigned)((n + tb - 1) / tb);
   if (ds->storage == CV_STORE_F32)
@@ -1358,8 +1359,6 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
     if (outs[q])
       CK(cudaMemcpyAsync(hosts[q], outs[q], sizeof(double) * n * per[q], cudaMemcpyDeviceToHost, ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
-  for (int q = 0; q < 5; ++q)
-    if (outs[q]) CK(cudaFree(outs[q]));
   return CV_OK;
 }
 
