@@ -261,6 +261,84 @@ __device__ __forceinline__ double rel_delta_t(const double* nw, const double* ol
   return md / fmax(mo, 1e-300);
 }
 
+// spd_inv_logdet_t across one warp (operands in shared memory): the same per-element
+// arithmetic in the same order (Cholesky column j by rows, L^-1 by columns, S = M^T M by
+// entries), so the result is bit-identical to the single-thread version.  Used by the
+// tail for d > 8, where the serial O(d^3) chain dominated the sweep tail.
+template <int D>
+__device__ bool chol_warp(const double* A, double* L, int lane) {
+  __shared__ double s_rl;
+  __shared__ int s_ok;
+  for (int i = lane; i < D * D; i += 32) L[i] = 0.0;
+  __syncwarp();
+  for (int j = 0; j < D; ++j) {
+    if (lane == 0) {
+      double s = A[j * D + j];
+      for (int k = 0; k < j; ++k) s -= L[j * D + k] * L[j * D + k];
+      s_ok = s > 0.0;
+      if (s_ok) {
+        const double ljj = sqrt(s);
+        s_rl = 1.0 / ljj;
+        L[j * D + j] = ljj;
+      }
+    }
+    __syncwarp();
+    if (!s_ok) return false;
+    const double rl = s_rl;
+    const int i = j + 1 + lane;
+    if (i < D) {
+      double t = A[i * D + j];
+      for (int k = 0; k < j; ++k) t -= L[i * D + k] * L[j * D + k];
+      L[i * D + j] = t * rl;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+template <int D>
+__device__ bool spd_inv_logdet_warp(double* A, double* Ainv, double* logdet, double* L, double* M, int lane) {
+  if (!chol_warp<D>(A, L, lane)) {
+    __shared__ double s_jit;
+    if (lane == 0) {
+      double tr = 0.0;
+      for (int j = 0; j < D; ++j) tr += A[j * D + j];
+      s_jit = 1e-10 * tr / D;
+    }
+    __syncwarp();
+    if (lane < D) A[lane * D + lane] += s_jit;  // the jitter-once retry (linalg.py:279-298)
+    __syncwarp();
+    if (!chol_warp<D>(A, L, lane)) return false;
+  }
+  for (int i = lane; i < D * D; i += 32) M[i] = 0.0;
+  __syncwarp();
+  if (lane < D) {  // column j = lane of L^-1
+    const int j = lane;
+    M[j * D + j] = 1.0 / L[j * D + j];
+    for (int i = j + 1; i < D; ++i) {
+      double t = 0.0;
+      for (int k = j; k < i; ++k) t -= L[i * D + k] * M[k * D + j];
+      M[i * D + j] = t / L[i * D + i];
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double prod = 1.0;
+    for (int j = 0; j < D; ++j) prod *= L[j * D + j];
+    *logdet = 2.0 * log(prod);
+  }
+  for (int e = lane; e < D * D; e += 32) {
+    const int i = e / D, j = e % D;
+    if (j < i) continue;
+    double t = 0.0;
+    for (int k = j; k < D; ++k) t += M[k * D + i] * M[k * D + j];
+    Ainv[i * D + j] = t;
+    Ainv[j * D + i] = t;
+  }
+  __syncwarp();
+  return true;
+}
+
 // ------------------------------------------------------------------ setup of the constants
 static __device__ __noinline__ void hyp_setup(Hyp& h) {
   const int d = h.d;
@@ -492,7 +570,10 @@ static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
 // (not its flops) are what the sweep pays for.
 template <int D>
 __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* stats, const double* Tm,
-                                       const double* hv) {
+                                       const double* hv, const double* preL = nullptr, const double* preS = nullptr,
+                                       double preld = 0.0, int pre_ok = 1) {
+  // preL / preS / preld: the new lam0l_inv, its inverse and log-det from the warp (tail_kernel,
+  // d > 8, sweep mode); otherwise computed here
   // Tm / hv: Ainv G Ainv and Ainv g of this pass (pass_products_t; the warp computes them in
   // tail_kernel, a batched thread for itself)
   constexpr int NS = n_stats(D);
@@ -564,17 +645,26 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
       dlt[i] = (hv[i] + h.q0 * k0c[i]) * rqv;
       k_new[i] = gen.c[i] + dlt[i];
     }
+    if (preL) {
 #pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = i; j < D; ++j) {
-        const double v =
-            h.L0inv[i * D + j] + h.V * Ai[i * D + j] + ((const volatile double*)Tm)[i * D + j] + h.q0 * k0c[i] * k0c[j] -
-            h.qv * dlt[i] * dlt[j];
-        L[i * D + j] = v;
-        L[j * D + i] = v;
+      for (int i = 0; i < D * D; ++i) {
+        L[i] = preL[i];
+        S[i] = preS[i];
       }
-    if (!finite || !spd_inv_logdet_t<D>(L, S, &ld)) status = CV_ERR_NUMERIC;  // rate inversion failed
+      ld = preld;
+      if (!finite || !pre_ok) status = CV_ERR_NUMERIC;  // rate inversion failed
+    } else {
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = i; j < D; ++j) {
+          const double v = h.L0inv[i * D + j] + h.V * Ai[i * D + j] + ((const volatile double*)Tm)[i * D + j] +
+                           h.q0 * k0c[i] * k0c[j] - h.qv * dlt[i] * dlt[j];
+          L[i * D + j] = v;
+          L[j * D + i] = v;
+        }
+      if (!finite || !spd_inv_logdet_t<D>(L, S, &ld)) status = CV_ERR_NUMERIC;  // rate inversion failed
+    }
     a = pend_a;
     b = pend_b;
     e_rho = gen.e_rho;

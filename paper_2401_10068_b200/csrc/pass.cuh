@@ -330,10 +330,47 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
       }
     __syncwarp();
   }
+  // d > 8, sweep mode: the new lam0l_inv and its Cholesky inverse across the warp too
+  constexpr bool kWarpInv = D > 8;
+  __shared__ double sL[kWarpInv ? D * D : 1], sS[kWarpInv ? D * D : 1], sC[kWarpInv ? D * D : 1],
+      sM[kWarpInv ? D * D : 1], sld;
+  __shared__ int sok;
+  const bool warp_inv = kWarpInv && mode == MODE_SWEEP;
+  if constexpr (kWarpInv) {
+    if (warp_inv) {
+      const Hyp& hh = *h;
+      const double rqv = 1.0 / hh.qv;
+      const int i = threadIdx.x;
+      if (i < D) {  // row i of L = L0inv + V Ainv + Ainv G Ainv + q0 k0c k0c^T - qv dlt dlt^T
+        const double k0ci = hh.K0[i] - c->pass.c[i];
+        const double dlti = (shv[i] + hh.q0 * k0ci) * rqv;
+        for (int j = 0; j < D; ++j) {
+          const double k0cj = hh.K0[j] - c->pass.c[j];
+          const double dltj = (shv[j] + hh.q0 * k0cj) * rqv;
+          const int a = i < j ? i : j, b = i < j ? j : i;  // the upper-triangle formula, as the serial code
+          const double ka = a == i ? k0ci : k0cj, kb = b == j ? k0cj : k0ci;
+          const double da = a == i ? dlti : dltj, db = b == j ? dltj : dlti;
+          sL[i * D + j] = hh.L0inv[a * D + b] + hh.V * sA[a * D + b] + sT[a * D + b] + hh.q0 * ka * kb - hh.qv * da * db;
+        }
+      }
+      __syncwarp();
+      for (int e = threadIdx.x; e < D * D; e += 32) sC[e] = sL[e];  // the inverse works on a copy
+      __syncwarp();
+      double ld = 0.0;
+      const bool ok = spd_inv_logdet_warp<D>(sC, sS, &ld, sM, sA, threadIdx.x);  // sA is free by now
+      if (threadIdx.x == 0) {
+        sld = ld;
+        sok = ok ? 1 : 0;
+      }
+      __syncwarp();
+    }
+  }
   if (threadIdx.x == 0) TAIL_PROF(*c, 6);
   if (threadIdx.x == 0) {
     if (mode == MODE_EM)
       em_tail_t<D>(*h, *c, tot);
+    else if (warp_inv)
+      tail_t<D>(*h, *c, tot, sT, shv, sL, sS, sld, sok);
     else
       tail_t<D>(*h, *c, tot, sT, shv);
   }
