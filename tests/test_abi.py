@@ -59,3 +59,18 @@ def test_product_has_no_cpu_fallback(monkeypatch, tmp_path):
         _lib.load(str(tmp_path / "missing.so"))
     src = open(os.path.join(ROOT, "paper_2401_10068_b200", "vb.py")).read()
     assert "oracle" not in src
+
+
+def test_status_codes_match_header():
+    """_lib's exception mapping uses the header's status values (cavi.h enum)."""
+    import re
+
+    from paper_2401_10068_b200 import _lib
+
+    with open(os.path.join(ROOT, "include", "cavi.h")) as fh:
+        text = fh.read()
+    codes = {m.group(1): int(m.group(2)) for m in re.finditer(r"(CV_(?:OK|ERR_\w+))\s*=\s*(\d+)", text)}
+    want = {"CV_OK": _lib.OK, "CV_ERR_NUMERIC": _lib.ERR_NUMERIC, "CV_ERR_NONFINITE": _lib.ERR_NONFINITE,
+            "CV_ERR_ARG": _lib.ERR_ARG, "CV_ERR_CUDA": _lib.ERR_CUDA, "CV_ERR_IMPROPER": _lib.ERR_IMPROPER,
+            "CV_ERR_FORMAT": _lib.ERR_FORMAT}
+    assert codes == want
