@@ -14,8 +14,8 @@
 // Kernel (sm_100a, persistent, 2-3 CTAs per SM): a producer warp streams the CTA's
 // chunks (dynamic tickets) tile by tile into a ring of shared-memory stages with TMA
 // bulk copies (cp.async.bulk + mbarrier complete_tx, L2 evict-first for streams larger
-// than L2); 4 consumer warps compute out of shared memory (d <= 5: one gene per thread
-// in registers; d >= 6: fp64 tensor cores, MmaConsumer) and release stages through
+// than L2); 4 consumer warps compute out of shared memory (d <= 7: one gene per thread
+// in registers; d >= 8: fp64 tensor cores, MmaConsumer) and release stages through
 // "empty" mbarriers.  The thread->gene map inside a chunk is fixed, so each chunk
 // partial is bit-reproducible whatever CTA computes it.  Chunk partials -> group (64
 // chunks) -> octants -> pairwise tree over the octants, each level by whichever warp
@@ -152,6 +152,69 @@ __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const dou
   for (int j = 0; j < D; ++j) acc[j] = fma(w, Dv[j], acc[j]);
 #pragma unroll
   for (int p = 0; p < D * (D + 1) / 2; ++p) acc[D + p] = fma(gam, P[p], acc[D + p]);
+  return den;
+}
+
+// gene<D>() with the symmetric forms factored by row: s = sum_j D_j (sum_{q>=j} A2_jq D_q)
+// (d independent chains instead of one d(d+1)/2-deep chain) and G_jq += (gam D_j) D_q, so
+// the d(d+1)/2 products D_j D_q are never held across the 1/den chain (d = 6 on the
+// register path: 9 fp64 ops fewer per gene and no spills at 2 CTAs/SM).  Same algebra,
+// different rounding order: only the streaming pass at d >= CAVI_ROWFORM_MIN_D uses it
+// (the batched kernel keeps gene<D>()).
+// Coefficients in registers (RegCoef) or, where registers run out (d >= 7), in a per-warp
+// shared-memory copy read per use (SmemCoef: volatile, so the loads are not hoisted back
+// into registers; every lane reads the same address, a broadcast).
+template <int D>
+struct RegCoef {
+  const GeneCoef<D>& k;
+  __device__ __forceinline__ double c(int j) const { return k.c[j]; }
+  __device__ __forceinline__ double a2(int p) const { return k.A2[p]; }
+  __device__ __forceinline__ double erho() const { return k.erho; }
+};
+template <int D>
+struct SmemCoef {
+  const volatile GeneCoef<D>* k;
+  double er;
+  __device__ __forceinline__ double c(int j) const { return k->c[j]; }
+  __device__ __forceinline__ double a2(int p) const { return k->A2[p]; }
+  __device__ __forceinline__ double erho() const { return er; }
+};
+
+template <int D, typename CK>
+__device__ __forceinline__ double gene_rows(const CK& k, double x, const double (&Dv)[D],
+                                            double (&acc)[n_stats(D)]) {
+  double t = 0.0, s = 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) t = fma(k.c(j), Dv[j], t);
+  {
+    int p = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double r = 0.0;
+#pragma unroll
+      for (int q = j; q < D; ++q) r = fma(k.a2(p++), Dv[q], r);
+      s = fma(Dv[j], r, s);
+    }
+  }
+  const double erho = k.erho();
+  const double den = fma(erho, s, 1.0);
+  const double inv = ptx::rcp_nr(den);
+  const double xt = x - t;
+  const double ei = erho * inv;
+  const double w = ei * xt;
+  const double gam = fma(w, w, -ei);
+  const double e = fma(-s, w, xt);
+  acc[stat_R(D)] += fma(e, e, s * inv);
+  acc[stat_Q(D)] = fma(w, xt, acc[stat_Q(D)]);
+#pragma unroll
+  for (int j = 0; j < D; ++j) acc[j] = fma(w, Dv[j], acc[j]);
+  int p = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const double gd = gam * Dv[j];
+#pragma unroll
+    for (int q = j; q < D; ++q, ++p) acc[D + p] = fma(gd, Dv[q], acc[D + p]);
+  }
   return den;
 }
 
@@ -724,6 +787,15 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 // CTA -> 0.489 ms/pass = 100% of the measured copy bandwidth.  (1 CTA x 8 warps x 4
 // genes/thread: 0.593 ms; 16 warps x 2 genes: 0.66 ms -- ILP per thread and two
 // independent pipelines per SM are what hides the fp64 latency chains.)
+#ifndef CAVI_ROWFORM_MIN_D
+#define CAVI_ROWFORM_MIN_D 4  // register path: gene_rows<D>() from this d up (N=5: 1524 -> 1570, N=6: 1245 -> 1340)
+#endif
+#ifndef CAVI_GENE_UNROLL_HI
+#define CAVI_GENE_UNROLL_HI 1  // register path, d >= 7: genes in flight per thread (d=7: 771 vs 757 at 2)
+#endif
+#ifndef CAVI_SMEM_COEF_MIN_D
+#define CAVI_SMEM_COEF_MIN_D 7  // register path: A^-1, c read from shared memory from this d up
+#endif
 #ifndef CAVI_CONS
 #define CAVI_CONS 128  // consumer threads per CTA (4 warps)
 #endif
@@ -741,7 +813,8 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #endif
 
 #ifndef CAVI_MMA_MIN_D
-#define CAVI_MMA_MIN_D 6  // smallest d served by the DMMA consumer (scalar d=6 spills: 424 vs 704 sweeps/s)
+#define CAVI_MMA_MIN_D 8  // smallest d served by the DMMA consumer (V=1e8 sweeps/s, register vs DMMA:
+                          // d=6 1038 vs 695, d=7 771 vs 677, d=8 565 vs 646)
 #endif
 #ifndef CAVI_MMA_SMALL_MAXD
 #define CAVI_MMA_SMALL_MAXD 9  // largest d run at CAVI_MMA_SMALL_BLOCKS CTAs/SM (d=10,11 spill at 3)
@@ -878,12 +951,19 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
   }
 
   // ---------------- consumers: independent warps, no CTA barrier in the steady state
-  GeneCoef<(G::kMma ? 1 : D)> k;
+  constexpr bool kSmemCoef = !G::kMma && D >= CAVI_SMEM_COEF_MIN_D;
+  __shared__ GeneCoef<kSmemCoef ? D : 1> s_coef[kSmemCoef ? kWarps : 1];
+  GeneCoef<(G::kMma || kSmemCoef ? 1 : D)> k;
   MmaConsumer<D> mc;
-  if constexpr (G::kMma)
+  if constexpr (G::kMma) {
     mc.load(ctl->pass, lane);
-  else
+  } else if constexpr (kSmemCoef) {
+    if (lane == 0) load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&s_coef[warp]), ctl->pass);
+    __syncwarp();
+  } else {
     load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&k), ctl->pass);
+  }
+  const double k_erho = ctl->pass.e_rho;
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
   uint32_t parity = 0;
@@ -919,13 +999,20 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
         if (t) ptx::mbar_wait(&full[stage], parity);
         const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
         double prod = 1.0;
-#pragma unroll
+        constexpr int kGU = D >= 7 ? CAVI_GENE_UNROLL_HI : G::kGenesPerThread;
+#pragma unroll kGU
         for (int u = 0; u < G::kGenesPerThread; ++u) {
           const int gi = u * kThreads + tid;
           double Dv[D];
 #pragma unroll
           for (int j = 0; j < D; ++j) Dv[j] = (double)tile[(j + 1) * G::kColStride + gi];
-          prod *= gene<D>(*reinterpret_cast<const GeneCoef<D>*>(&k), (double)tile[gi], Dv, acc);
+          if constexpr (kSmemCoef)
+            prod *= gene_rows<D>(SmemCoef<D>{reinterpret_cast<const volatile GeneCoef<D>*>(&s_coef[warp]), k_erho},
+                                 (double)tile[gi], Dv, acc);
+          else if constexpr (D >= CAVI_ROWFORM_MIN_D)
+            prod *= gene_rows<D>(RegCoef<D>{*reinterpret_cast<const GeneCoef<D>*>(&k)}, (double)tile[gi], Dv, acc);
+          else
+            prod *= gene<D>(*reinterpret_cast<const GeneCoef<D>*>(&k), (double)tile[gi], Dv, acc);
         }
         lg.mul(prod);
         __syncwarp();
