@@ -790,9 +790,6 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_ROWFORM_MIN_D
 #define CAVI_ROWFORM_MIN_D 4  // register path: gene_rows<D>() from this d up (N=5: 1524 -> 1570, N=6: 1245 -> 1340)
 #endif
-#ifndef CAVI_GENE_UNROLL_HI
-#define CAVI_GENE_UNROLL_HI 1  // register path, d >= 7: genes in flight per thread (d=7: 771 vs 757 at 2)
-#endif
 #ifndef CAVI_SMEM_COEF_MIN_D
 #define CAVI_SMEM_COEF_MIN_D 7  // register path: A^-1, c read from shared memory from this d up
 #endif
@@ -999,8 +996,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
         if (t) ptx::mbar_wait(&full[stage], parity);
         const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
         double prod = 1.0;
-        constexpr int kGU = D >= 7 ? CAVI_GENE_UNROLL_HI : G::kGenesPerThread;
-#pragma unroll kGU
+#pragma unroll
         for (int u = 0; u < G::kGenesPerThread; ++u) {
           const int gi = u * kThreads + tid;
           double Dv[D];
