@@ -103,6 +103,7 @@ def test_generator_matches_oracle(eng, V, N, seed):
 
 
 @pytest.mark.parametrize("N,V,iters", [(3, 4000, 40), (4, 50000, 25), (2, 10000, 30), (6, 3000, 15),
+                                       (7, 40000, 10), (8, 3000, 10), (9, 2000, 8),  # register/DMMA boundary
                                        (12, 2000, 8), (16, 3000, 6)])
 def test_fit_matches_direct_oracle(eng, N, V, iters):
     vb, model = eng
@@ -128,11 +129,12 @@ def test_device_dataset_equals_uploaded(eng):
     assert np.array_equal(s1.k0k, s2.k0k)
 
 
-def test_fp32_storage_within_1e4(eng):
+@pytest.mark.parametrize("N", [4, 7, 8])
+def test_fp32_storage_within_1e4(eng, N):
     vb, model = eng
-    dd64 = model.regime(200000, 3, 4)
-    dd32 = model.regime(200000, 3, 4, storage="f32")
-    hp = model.default_hyperparams(4)
+    dd64 = model.regime(200000, 3, N)
+    dd32 = model.regime(200000, 3, N, storage="f32")
+    hp = model.default_hyperparams(N)
     s64, t64 = vb.vb_fit(dd64, hp, max_iter=40, rel_tol=0.0)
     s32, t32 = vb.vb_fit(dd32, hp, max_iter=40, rel_tol=0.0)
     np.testing.assert_allclose(t32.elbo, t64.elbo, rtol=1e-4)
