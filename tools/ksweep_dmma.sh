@@ -1,6 +1,6 @@
 # K sweep of the fused pass at V=1e8 (config 5): one bench line per N
 for N in "$@"; do
-  timeout 300 python bench.py --networks $N --steps 30 --warmup 5 --no-e2e --no-cpu > gpurun_out/ks_$N.json 2> gpurun_out/ks_$N.err
+  timeout 300 python bench.py --networks $N --steps 30 --warmup 5 --no-e2e --no-cpu --no-converge > gpurun_out/ks_$N.json 2> gpurun_out/ks_$N.err
   python - "$N" <<'PY'
 import json, sys
 N = sys.argv[1]
