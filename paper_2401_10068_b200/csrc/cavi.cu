@@ -125,6 +125,7 @@ struct cv_dataset {
   cudaGraphExec_t graph = nullptr;
   int graph_unroll = 0;
   Ctl* h_ctl = nullptr;  // pinned mirror
+  int* h_done = nullptr;  // pinned [2]: done flags of the last two sweep groups (cv_fit)
   int bad_input = 0;
   size_t device_bytes = 0;
   unsigned long long* cta_trace = nullptr;  // CAVI_TRACE_CTA diagnostics
@@ -236,6 +237,7 @@ int plan_and_alloc(cv_dataset* ds) {
   PALLOC(ds->ctl, sizeof(Ctl));
   PALLOC(ds->hyp, sizeof(Hyp));
   CK(cudaMallocHost(&ds->h_ctl, sizeof(Ctl)));
+  CK(cudaMallocHost(&ds->h_done, 2 * sizeof(int)));
   for (auto& e : ds->ev) CK(cudaEventCreate(&e));
   ds->device_bytes = nx * es * (1 + ds->d);
   ds->pass = pass_for(ds->d, ds->storage);
@@ -662,6 +664,7 @@ void cv_dataset_destroy(cv_dataset* ds) {
   for (void* b : plain)
     if (b) cudaFree(b);
   if (ds->h_ctl) cudaFreeHost(ds->h_ctl);
+  if (ds->h_done) cudaFreeHost(ds->h_done);
   for (auto e : ds->ev)
     if (e) cudaEventDestroy(e);
   if (ds->stream) cudaStreamDestroy(ds->stream);
@@ -1216,15 +1219,26 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
   // sweeps: unrolled graphs; every pass kernel exits at once after the stop rule fired
   const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
   if ((rc = ensure_graph(ds, unroll))) return rc;
+  // Two groups in flight: group k+1 is queued before the host reads group k's done flag,
+  // so the device never idles on the host round trip.  After the stop rule fires, the one
+  // extra group's kernels all exit at once (they read ctl->done first).
   int launched = 0;
-  for (;;) {
+  auto enqueue = [&](int b) -> int {
     CK(cudaGraphLaunch(ds->graph, ds->stream));
     launched += unroll;
-    CK(cudaMemcpyAsync(&ds->h_ctl->done, &ds->ctl->done, sizeof(int) * 4, cudaMemcpyDeviceToHost, ds->stream));
-    CK(cudaStreamSynchronize(ds->stream));
-    if (ds->h_ctl->done || launched >= max_iter) break;
+    CK(cudaMemcpyAsync(&ds->h_done[b], &ds->ctl->done, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaEventRecord(ds->ev[2 + b], ds->stream));
+    return CV_OK;
+  };
+  if ((rc = enqueue(0))) return rc;
+  for (int k = 0;; ++k) {
+    const int b = k & 1;
+    const bool more = launched < max_iter;
+    if (more && (rc = enqueue(1 - b))) return rc;
+    CK(cudaEventSynchronize(ds->ev[2 + b]));
+    if (ds->h_done[b] || !more) break;
   }
-  if ((rc = ctl_get(ds))) return rc;
+  if ((rc = ctl_get(ds))) return rc;  // stream-ordered after the extra group
   const Ctl& h = *ds->h_ctl;
   *out = h.cur;
   *n_iter = h.iter;
