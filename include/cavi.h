@@ -46,7 +46,8 @@ enum {
   CV_ERR_ARG = 3,
   CV_ERR_CUDA = 4,
   CV_ERR_IMPROPER = 5, /* NumericError("Q(Lambda) is improper; dataset too small") */
-  CV_ERR_FORMAT = 6    /* cli.UsageError: malformed dataset file (header / field count) */
+  CV_ERR_FORMAT = 6,   /* cli.UsageError: malformed dataset file (header / field count) */
+  CV_ERR_PEER = 7      /* multi-GPU: a peer's statistics did not arrive within CAVI_PEER_TIMEOUT_S */
 };
 
 /* storage layouts of the measurement stream in HBM */
@@ -140,7 +141,10 @@ void cv_dataset_destroy(cv_dataset* ds);
  * Python planner `dist.shard_ranges` computes).  Per sweep the ranks exchange
  * one n_stats(d)-double partial (ncclAllGather) and all run the identical tail,
  * so states, traces and stop decisions agree bit-for-bit on every rank, and
- * with the single-GPU result for any world size. */
+ * with the single-GPU result for any world size.  Every shard call (cv_init, cv_step,
+ * cv_elbo, cv_fit, cv_em_*) begins with a collective (an NCCL allreduce used as a barrier
+ * and to resync the fused exchange's sequence counter), so all ranks must make the same
+ * shard calls in the same order, as with any NCCL collective. */
 int32_t cv_nccl_unique_id(uint8_t* out /* 128 bytes */);
 int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t device, cv_comm** out);
 void cv_comm_destroy(cv_comm* c);
@@ -148,6 +152,10 @@ void cv_comm_destroy(cv_comm* c);
  * NVLink, checked by a collective self-test at cv_comm_create); 0: ncclAllGather per sweep.
  * CAVI_NO_LSA=1 forces the NCCL path; a world of one uses neither (CAVI_LSA_WORLD1=1: fused). */
 int32_t cv_comm_fused(cv_comm* c);
+/* Fault injection (tests): this rank skips publishing its partial `ahead` sweeps after the
+ * next shard call's entry resync, so every rank's tail times out (CV_ERR_PEER after
+ * CAVI_PEER_TIMEOUT_S).  The following shard call resyncs and runs normally. */
+int32_t cv_comm_drop_publish(cv_comm* c, int32_t ahead);
 int32_t cv_dataset_set_comm(cv_dataset* ds, cv_comm* comm);
 /* Mark a shard as rank `rank` of `world` without a communicator (single-GPU
  * emulation of the multi-GPU reduction for tests) and return the shard's

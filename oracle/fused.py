@@ -165,6 +165,26 @@ def full_stats(x, D, gen: Generator):
     return tree8(octs)
 
 
+def streamed_stats(x, D, gen: Generator):
+    """full_stats with memory bounded by one group: the per-gene terms are formed one group
+    (GROUP_CHUNKS chunks) at a time, so the plan runs at V = 1e8-1e9 on a host (the same
+    chunk -> group -> octant -> tree8 sums as local_stats)."""
+    V = x.shape[0]
+    p = make_plan(V)
+    ns = n_stats(D.shape[1])
+    step = GROUP_CHUNKS * CHUNK_GENES
+    gsums = []
+    for g0 in range(0, V, step):
+        hi = min(g0 + step, V)
+        t = gene_terms(x[g0:hi], D[g0:hi], gen)
+        gsums.append(warp_rows_sum([t[c0:c0 + CHUNK_GENES].sum(axis=0) for c0 in range(0, hi - g0, CHUNK_GENES)]))
+    octs = []
+    for o in range(N_OCTANTS):
+        a, b = o * p.groups_per_octant, min((o + 1) * p.groups_per_octant, p.n_groups)
+        octs.append(warp_rows_sum(gsums[a:b]) if b > a else np.zeros(ns))
+    return tree8(octs)
+
+
 def rank_partial(x_all, D_all, gen: Generator, rank: int, world: int):
     """The partial rank `rank` of `world` contributes (its octant subtree)."""
     V = x_all.shape[0]
@@ -276,10 +296,13 @@ def rel_delta(new, old):
     return float(np.max(np.abs(np.asarray(new) - np.asarray(old)))) / den
 
 
-def fit(r, mu, D, hp: Hyper, max_iter=300, rel_tol=1e-8, compute_elbo=True, param_tol=1e-10):
-    """Single-pass CAVI fit; returns (Globals, trace dict, n_iter)."""
+def fit(r, mu, D, hp: Hyper, max_iter=300, rel_tol=1e-8, compute_elbo=True, param_tol=1e-10, x=None,
+        stats_fn=None):
+    """Single-pass CAVI fit; returns (Globals, trace dict, n_iter).  `x` = r - mu if already
+    formed; `stats_fn` = streamed_stats for datasets too large to hold the per-gene terms."""
     V = D.shape[0]
-    x = r - mu
+    x = r - mu if x is None else x
+    full_stats = stats_fn or globals()["full_stats"]
     gen, st = init(hp, V)
     resid = float(full_stats(x, D, gen)[-3])
     es, dk, dr, dl = [], [], [], []

@@ -16,7 +16,7 @@ from . import linalg
 MAX_D = 15
 MAX_D2 = MAX_D * MAX_D
 
-OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT = range(7)
+OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT, ERR_PEER = range(8)
 STORE_F64, STORE_F32 = 0, 1
 
 _LIB_PATH = os.environ.get("CAVI_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcavi.so"))
@@ -87,6 +87,7 @@ _SIGS = {
     "cv_comm_create": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "cv_comm_destroy": (None, [C.c_void_p]),
     "cv_comm_fused": (C.c_int32, [C.c_void_p]),
+    "cv_comm_drop_publish": (C.c_int32, [C.c_void_p, C.c_int32]),
     "cv_dataset_set_comm": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "cv_dataset_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
     "cv_shard_stats": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), _D]),
@@ -144,6 +145,11 @@ class UsageError(ValueError):
     """A malformed dataset file (the reference's cli.UsageError, cli.py:40-41)."""
 
 
+class PeerTimeoutError(RuntimeError):
+    """Multi-GPU: a peer's per-sweep statistics did not arrive within CAVI_PEER_TIMEOUT_S
+    (a stalled or failed rank).  The next shard call resyncs the communicator."""
+
+
 def check(rc: int) -> None:
     """Map a status code to the reference's exception types (linalg.py:46-69)."""
     if rc == OK:
@@ -157,6 +163,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == ERR_FORMAT:
         raise UsageError(msg)
+    if rc == ERR_PEER:
+        raise PeerTimeoutError(msg)
     raise RuntimeError(f"libcavi: {msg}")
 
 

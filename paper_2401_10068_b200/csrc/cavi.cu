@@ -90,7 +90,10 @@ struct cv_comm {
   // fused exchange (lsa.cuh): symmetric window of the NCCL device API + sequence counter
   void* sym = nullptr;
   ncclWindow_t win = nullptr;
-  unsigned long long* seq = nullptr;
+  unsigned long long* seq = nullptr;  // [0] sequence counter, [1] injected-fault sequence (lsa.cuh)
+  unsigned long long* entry = nullptr;  // [1] scratch of the entry collective (shard_entry)
+  unsigned long long timeout_ns = 10000000000ull;  // CAVI_PEER_TIMEOUT_S
+  int drop_ahead = 0;  // cv_comm_drop_publish, applied at the next shard_entry
   int lsa = 0;  // 1: the pass publishes into peers' windows; 0: ncclAllGather
 };
 
@@ -250,8 +253,9 @@ int plan_and_alloc(cv_dataset* ds) {
 }
 
 LsaLink lsa_link(const cv_dataset* ds) {
-  LsaLink L{nullptr, nullptr, 1, 0};
-  if (ds->comm && ds->comm->lsa) L = LsaLink{ds->comm->win, ds->comm->seq, ds->comm->world, ds->comm->rank};
+  LsaLink L{nullptr, nullptr, 1, 0, 0};
+  if (ds->comm && ds->comm->lsa)
+    L = LsaLink{ds->comm->win, ds->comm->seq, ds->comm->world, ds->comm->rank, ds->comm->timeout_ns};
   return L;
 }
 
@@ -339,8 +343,8 @@ void lsa_setup(cv_comm* c) {
   if (ok && ncclTeamLsa(c->nccl).nRanks != c->world) ok = 0;  // one NVLink domain only
   if (ok && ncclMemAlloc(&c->sym, kLsaWindowBytes) != ncclSuccess) ok = 0;
   if (ok && cudaMemset(c->sym, 0, kLsaWindowBytes) != cudaSuccess) ok = 0;
-  if (ok && cudaMalloc(&c->seq, sizeof(unsigned long long)) != cudaSuccess) ok = 0;
-  if (ok && cudaMemset(c->seq, 0, sizeof(unsigned long long)) != cudaSuccess) ok = 0;
+  if (ok && cudaMalloc(&c->seq, 2 * sizeof(unsigned long long)) != cudaSuccess) ok = 0;
+  if (ok && cudaMemset(c->seq, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) ok = 0;
   ok = agree(c, dflag, ok);
   if (ok && ncclCommWindowRegister(c->nccl, c->sym, kLsaWindowBytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) {
     c->win = nullptr;
@@ -349,7 +353,7 @@ void lsa_setup(cv_comm* c) {
   ok = agree(c, dflag, ok);
   if (ok) {
     cudaMemset(dflag + 1, 0, sizeof(int));
-    lsa_selftest_kernel<<<1, 32>>>(LsaLink{c->win, c->seq, c->world, c->rank}, 1ull, dflag + 1);
+    lsa_selftest_kernel<<<1, 32>>>(LsaLink{c->win, c->seq, c->world, c->rank, c->timeout_ns}, 1ull, dflag + 1);
     int got = 0;
     if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(&got, dflag + 1, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
       got = 0;
@@ -404,6 +408,37 @@ int launch_tail_only(cv_dataset* ds) {
 int launch_pass(cv_dataset* ds) {
   int rc = launch_pass_only(ds);
   return rc ? rc : launch_tail_only(ds);
+}
+
+// Every shard call starts with this collective: an NCCL allreduce that is a
+// barrier -- ranks reach the first exchange together, so the tail's bounded wait measures the
+// exchange, not host skew (uneven ingest, uploads, Python work) -- and, on the fused path,
+// resyncs the sequence counter to (max over ranks) + 2, a tag no word left in any window by an
+// earlier exchange (even one that timed out on some ranks) can carry.
+int shard_entry(cv_dataset* ds) {
+  cv_comm* c = ds->comm;
+  if (!c) return CV_OK;
+  if (!c->entry) CK(cudaMalloc(&c->entry, sizeof(unsigned long long)));
+  if (c->lsa)
+    CK(cudaMemcpyAsync(c->entry, c->seq, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, ds->stream));
+  else
+    CK(cudaMemsetAsync(c->entry, 0, sizeof(unsigned long long), ds->stream));
+  ncclResult_t r = ncclAllReduce(c->entry, c->entry, 1, ncclUint64, ncclMax, c->nccl, ds->stream);
+  if (r != ncclSuccess) return fail(CV_ERR_CUDA, "ncclAllReduce (shard entry): %s", ncclGetErrorString(r));
+  if (c->lsa) {
+    lsa_resync_kernel<<<1, 1, 0, ds->stream>>>(c->entry, c->seq);
+    CK(cudaGetLastError());
+    if (c->drop_ahead > 0) {  // fault injection: drop the publish of sweep seq + drop_ahead
+      unsigned long long m = 0;
+      CK(cudaMemcpyAsync(&m, c->entry, sizeof m, cudaMemcpyDeviceToHost, ds->stream));
+      CK(cudaStreamSynchronize(ds->stream));
+      const unsigned long long drop = m + 2 + (unsigned long long)c->drop_ahead;
+      CK(cudaMemcpyAsync(c->seq + 1, &drop, sizeof drop, cudaMemcpyHostToDevice, ds->stream));
+      c->drop_ahead = 0;
+    }
+  }
+  CK(cudaStreamSynchronize(ds->stream));
+  return CV_OK;
 }
 
 int check_hyper(cv_dataset* ds, const cv_hyper* hp) {
@@ -474,6 +509,9 @@ int status_code(int s) {
       return CV_OK;
     case CV_ERR_NUMERIC:
       return fail(CV_ERR_NUMERIC, "Q(Lambda) rate inversion failed after jitter retry (non-PD or non-finite)");
+    case CV_ERR_PEER:
+      return fail(CV_ERR_PEER, "peer exchange timed out: a rank's statistics did not arrive within "
+                               "CAVI_PEER_TIMEOUT_S (the next shard call resyncs the communicator)");
     default:
       return fail(s, "sweep failed with status %d", s);
   }
@@ -561,6 +599,10 @@ int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t d
   c->rank = rank;
   c->world = world;
   c->device = device;
+  if (const char* t = getenv("CAVI_PEER_TIMEOUT_S")) {
+    const double sec = atof(t);
+    if (sec > 0) c->timeout_ns = (unsigned long long)(sec * 1e9);
+  }
   ncclResult_t r = ncclCommInitRank(&c->nccl, world, uid, rank);
   if (r != ncclSuccess) {
     delete c;
@@ -573,9 +615,17 @@ int32_t cv_comm_create(const uint8_t* id, int32_t rank, int32_t world, int32_t d
 
 int32_t cv_comm_fused(cv_comm* c) { return c ? c->lsa : 0; }
 
+int32_t cv_comm_drop_publish(cv_comm* c, int32_t ahead) {
+  if (!c || ahead < 1) return fail(CV_ERR_ARG, "bad fault injection");
+  if (!c->lsa) return fail(CV_ERR_ARG, "fault injection needs the fused exchange");
+  c->drop_ahead = ahead;
+  return CV_OK;
+}
+
 void cv_comm_destroy(cv_comm* c) {
   if (!c) return;
   lsa_teardown(c);
+  if (c->entry) cudaFree(c->entry);
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
 }
@@ -1143,6 +1193,7 @@ int32_t cv_init(cv_dataset* ds, const cv_hyper* hp, cv_state* out) {
   if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_init on a shard needs cv_dataset_set_comm");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
+  if ((rc = shard_entry(ds))) return rc;
   rc = run_init(ds, 1);
   if (rc) return rc;
   rc = ctl_get(ds);
@@ -1158,6 +1209,7 @@ int32_t cv_step(cv_dataset* ds, const cv_hyper* hp, const cv_state* in, cv_state
   if (in->d != ds->d || in->V != ds->V_total) return fail(CV_ERR_ARG, "state does not belong to this dataset");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
+  if ((rc = shard_entry(ds))) return rc;
   Ctl c;
   reset_ctl(c);
   c.cur = *in;
@@ -1176,6 +1228,7 @@ int32_t cv_elbo(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, double* 
   if (st->d != ds->d || st->V != ds->V_total) return fail(CV_ERR_ARG, "state does not belong to this dataset");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
+  if ((rc = shard_entry(ds))) return rc;
   Ctl c;
   reset_ctl(c);
   c.cur = *st;
@@ -1200,6 +1253,7 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
   if (ds->V != ds->V_total && !ds->comm) return fail(CV_ERR_ARG, "cv_fit on a shard needs cv_dataset_set_comm");
   int rc = upload_hyper(ds, hp);
   if (rc) return rc;
+  if ((rc = shard_entry(ds))) return rc;
   if ((rc = ensure_trace(ds, max_iter))) return rc;
   Ctl c;
   reset_ctl(c);
@@ -1261,6 +1315,7 @@ static int em_setup(cv_dataset* ds, const double* K, const double* Lam, double r
   cv_hyper hp{1.0, 1.0, 1.0, 1, ds->d, K0.data(), L0.data()};
   int rc = upload_hyper(ds, &hp);
   if (rc) return rc;
+  if ((rc = shard_entry(ds))) return rc;
   if ((rc = ensure_trace(ds, std::max(trace_cap, 1)))) return rc;
   reset_ctl(c);
   c.max_iter = max_iter;

@@ -13,7 +13,11 @@
 // Double buffering is enough: rank A can only start pass s+2 after its tail s+1 saw every
 // rank's pass s+1, i.e. after every rank's tail s finished reading parity s & 1; stale
 // words of that parity carry sequence s-2, never s.
-// Every wait is bounded: a stalled peer ends the fit with an error, never a hung GPU.
+// Every wait is bounded (globaltimer deadline, CAVI_PEER_TIMEOUT_S, default 10 s): a
+// stalled peer ends the fit with CV_ERR_PEER, never a hung GPU.  After a timeout the ranks'
+// counters may disagree and the failed sweep's words stay in the windows; every shard call
+// therefore starts with a collective resync (cavi.cu shard_entry): seq := max over ranks + 2,
+// a tag no stale word can carry.
 #pragma once
 
 #include <nccl.h>
@@ -27,9 +31,17 @@ constexpr int kMaxNS = 15 + 15 * 16 / 2 + 3;  // n_stats(15)
 
 struct LsaLink {
   ncclWindow_t win;           // null: exchange through NCCL (or single GPU)
-  unsigned long long* seq;    // [1] sweeps exchanged so far (this rank's device memory)
+  unsigned long long* seq;    // [0] sweeps exchanged so far (this rank's device memory);
+                              // [1] fault injection (tests): the sequence whose publish is dropped, 0 = none
   int world, rank;            // LSA team == world (single NVLink domain)
+  unsigned long long timeout_ns;  // bound on the tail's wait for the peers' words
 };
+
+__device__ __forceinline__ unsigned long long lsa_now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr size_t lsa_data_off(int parity, int rank) {
   return ((size_t)(parity * kMaxRanks + rank) * kMaxNS * 2) * sizeof(uint64_t);
@@ -48,6 +60,7 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
 // One warp: publish this rank's ns statistics `val(st)` for sequence s to every peer.
 template <typename F>
 __device__ __forceinline__ void lsa_publish(const LsaLink& L, uint64_t s, int ns, F val, int lane) {
+  if (L.seq[1] == s) return;  // injected fault: this rank never publishes sweep s
   const int par = (int)(s & 1);
   const uint64_t tag = (uint64_t)(uint32_t)s << 32;
   for (int st = lane; st < ns; st += 32) {
@@ -62,14 +75,14 @@ __device__ __forceinline__ void lsa_publish(const LsaLink& L, uint64_t s, int ns
 }
 
 // Value of statistic st from rank r for sequence s, polled from this rank's window
-// (bounded by the clock deadline; *ok = false on timeout).
-__device__ __forceinline__ double lsa_take(const LsaLink& L, uint64_t s, int r, int st, long long deadline,
+// (bounded by the globaltimer deadline; *ok = false on timeout).
+__device__ __forceinline__ double lsa_take(const LsaLink& L, uint64_t s, int r, int st, unsigned long long deadline,
                                            bool* ok) {
   const uint32_t want = (uint32_t)s;
   const uint64_t* w = static_cast<const uint64_t*>(ncclGetLocalPointer(L.win, lsa_data_off((int)(s & 1), r))) + 2 * st;
   uint64_t a = ld_relaxed_sys(w), b = ld_relaxed_sys(w + 1);
   while ((uint32_t)(a >> 32) != want || (uint32_t)(b >> 32) != want) {
-    if (clock64() > deadline) {
+    if (lsa_now_ns() > deadline) {
       *ok = false;
       return 0.0;
     }
@@ -93,13 +106,19 @@ static __global__ void lsa_selftest_kernel(LsaLink L, uint64_t s, int* ok) {
   const int lane = threadIdx.x;
   lsa_publish(L, s, 32, [&](int st) { return 1000.0 * L.rank + st + 0.25 * (double)s; }, lane);
   bool good = true;
-  const long long deadline = clock64() + (1ll << 31);
+  const unsigned long long deadline = lsa_now_ns() + L.timeout_ns;
   for (int r = 0; r < L.world; ++r) {
     const double v = lsa_take(L, s, r, lane, deadline, &good);
     good = good && v == 1000.0 * r + lane + 0.25 * (double)s;
   }
   good = __all_sync(0xffffffffu, good);
   if (lane == 0) *ok = good ? 1 : 0;
+}
+
+// seq := (max over ranks, already in *m) + 2 -- the entry resync of every shard call
+static __global__ void lsa_resync_kernel(const unsigned long long* m, unsigned long long* seq) {
+  seq[0] = m[0] + 2ull;
+  seq[1] = 0ull;
 }
 
 }  // namespace cavi

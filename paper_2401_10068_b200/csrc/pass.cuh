@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
   if (*(volatile const int*)&c->done) return;
   if (lsa.win) {  // fused exchange: every rank's partial arrives in this rank's window
     const uint64_t s = *lsa.seq + 1;
-    const long long deadline = clock64() + (1ll << 33);  // ~4 s: a peer stalled -> error, not a hang
+    const unsigned long long deadline = lsa_now_ns() + lsa.timeout_ns;  // a stalled peer -> error, not a hang
     bool ok = true;
     for (int st = threadIdx.x; st < NS; st += 32) {
       double v[kOctants];
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
     }
     if (!__all_sync(0xffffffffu, ok)) {
       if (threadIdx.x == 0) {
-        c->status = CV_ERR_CUDA;
+        c->status = CV_ERR_PEER;
         c->done = 1;
       }
       return;

@@ -108,6 +108,11 @@ class Comm:
         peers' NCCL symmetric windows); False: one ncclAllGather per sweep."""
         return bool(_lib.lib().cv_comm_fused(self._h))
 
+    def drop_publish(self, ahead: int) -> None:
+        """Fault injection for tests: skip this rank's publish `ahead` sweeps into the next
+        shard call, so that call fails with PeerTimeoutError (cv_comm_drop_publish)."""
+        _lib.check(_lib.lib().cv_comm_drop_publish(self._h, int(ahead)))
+
     @classmethod
     def bootstrap(cls, device: int | None = None, td=None) -> "Comm":
         td = td or init_host_group()

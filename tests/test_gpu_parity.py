@@ -51,7 +51,7 @@ def test_fit_matches_reference_golden(eng, name):
     else:
         np.testing.assert_allclose(tr.elbo, g["elbo"], rtol=RTOL, atol=0)
     for k in ("delta_k0k", "delta_rho", "delta_lam"):
-        np.testing.assert_allclose(getattr(tr, k), g[k], rtol=1e-6, atol=1e-12, err_msg=k)
+        np.testing.assert_allclose(getattr(tr, k), g[k], rtol=RTOL, atol=1e-12, err_msg=k)
     assert st.a_rho == float(g["a_rho"])
     close(st.b_rho, g["b_rho"], what="b_rho")
     close(st.k0k, g["k0k"], what="k0k")
@@ -163,7 +163,7 @@ def test_batched_fits_match_reference_goldens(eng):
         g = gs[i % len(gs)]
         assert len(tr) == int(g["n_iter"])
         np.testing.assert_allclose(tr.elbo, g["elbo"], rtol=RTOL, atol=0)
-        np.testing.assert_allclose(tr.delta_k0k, g["delta_k0k"], rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(tr.delta_k0k, g["delta_k0k"], rtol=RTOL, atol=1e-12)
         close(st.k0k, g["k0k"])
         close(st.lam0l_inv, g["lam0l_inv"])
         close(st.b_rho, g["b_rho"])

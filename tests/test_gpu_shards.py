@@ -97,10 +97,12 @@ def test_fused_exchange_is_active_and_exact():
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         td.init_process_group("gloo", rank=0, world_size=1)
     os.environ["CAVI_LSA_WORLD1"] = "1"  # one GPU needs no exchange; run the protocol anyway
+    os.environ["CAVI_PEER_TIMEOUT_S"] = "0.5"
     try:
         comm = dist.Comm.bootstrap(device=0, td=td)
     finally:
         del os.environ["CAVI_LSA_WORLD1"]
+        del os.environ["CAVI_PEER_TIMEOUT_S"]
     assert comm.fused
     V, N = 600_000, 3
     K, lam = np.array([0.1, 0.3]), np.linalg.inv(model.REFERENCE_LAMBDA_INV)
@@ -110,3 +112,13 @@ def test_fused_exchange_is_active_and_exact():
     for _ in range(2):  # several fits: the sequence counter and parities keep advancing
         st, tr = vb.vb_fit(shard, hp, max_iter=80)
         assert np.array_equal(tr.elbo, ref_tr.elbo) and st.b_rho == ref_st.b_rho
+    # a rank that stops publishing mid-fit (fault injection: sweep 2's partial never lands):
+    # the tail's bounded wait ends the fit with PeerTimeoutError instead of hanging, and the
+    # next call's entry resync (seq := max + 2 over ranks) leaves no stale word usable
+    from paper_2401_10068_b200 import _lib
+
+    comm.drop_publish(3)  # init pass = entry + 1, sweep 1 = + 2, sweep 2 = + 3
+    with pytest.raises(_lib.PeerTimeoutError):
+        vb.vb_fit(shard, hp, max_iter=80)
+    st, tr = vb.vb_fit(shard, hp, max_iter=80)
+    assert np.array_equal(tr.elbo, ref_tr.elbo) and st.b_rho == ref_st.b_rho
