@@ -10,8 +10,9 @@ e2e    : the same metric through the public API, vb_fit(host Dataset) with
          the H2D upload of r, mu, D (from pinned memory) and the D2H of the
          result inside the timed region: iters / s = sweeps / wall of the call
 reference arm (--impl reference): the reference algorithm (oracle port of
-         tissuemix.vb, numpy, host cores) timed on a bounded sample of the
-         same workload and scaled to the full 1e8 genes.
+         tissuemix.vb, numpy) on every host core, one process per core over its
+         slice of the same dataset, W warm-up + K barrier-delimited timed sweeps
+         (the whole 1e8 genes when that fits ~150 s, else a prefix, scaled).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -126,91 +127,121 @@ def traffic_per_launch():
         return None
 
 
-# ----------------------------------------------------------------------------- CPU side
-def cpu_reference_sample(V_total, N, target_s=1.0, min_genes=20000):
-    """One sweep (vb_step + vb_elbo) of the reference algorithm (oracle port) on a sample.
+# ----------------------------------------------------------------------------- shared
+def bench_config(V, N, storage, world=1):
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    d = N - 1
+    esz = 8 if storage == "f64" else 4
+    nbytes = V * esz * (1 + d)
+    return {"workload": f"CAVI sweep (vb_step + vb_elbo) over V={V:.0e} genes, N={N} networks (d={d}), "
+                        f"seed-{SEED} synthetic dataset (K=0.2, Lambda=100 I, rho=100), {storage} "
+                        + ("on 1 GPU" if world == 1 else f"sharded by octant over {world} GPUs"),
+            "V": V, "N": N, "seed": SEED, "storage": storage,
+            "l2": (f"inputs ({nbytes / 1e9:.2f} GB) larger than L2 (126 MB); no flush needed" if nbytes > 126e6 else
+                   f"inputs ({nbytes / 1e6:.0f} MB) L2-resident by design (evict-last): the small-V latency "
+                   f"regime, not an HBM measurement"),
+            "parallelism": "single GPU" if world == 1 else f"dp{world} (gene shards)"}
 
-    Returns a closure timing one sweep, plus the sample description.
-    """
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            names = [ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")]
+        return f"{names[0]} x {len(names)} logical CPUs"
+    except Exception:
+        return "unknown"
+
+
+# ----------------------------------------------------------------------------- CPU side
+def _mem_available():
+    try:
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
+
+
+def _ref_worker(args):
+    """One host process: genes [lo, hi) of the seed-2026 dataset, the reference algorithm
+    (oracle port of tissuemix.vb: vb_step then vb_elbo) once per barrier-delimited step."""
+    lo, hi, V_total, N, n_steps, barrier, q = args
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
     from oracle import cavi as ocavi  # the reference's algorithm restated (reported baseline only)
     from oracle import philox
 
     K, Lam, rho = truth(N)
-    # probe: size the sample so one sweep takes ~target_s
-    Vs = min_genes
-    r, mu, D = philox.generate(SEED, Vs, N, K, Lam, rho)
+    r, mu, D = philox.generate_slice(SEED, lo, hi, V_total, N, K, Lam, rho)
     hp = ocavi.default_hyper(N)
     st = ocavi.init(r, mu, D, hp)
-    t0 = time.perf_counter()
-    ocavi.elbo(ocavi.step(st, r, mu, D, hp), r, mu, D, hp)
-    per_gene = (time.perf_counter() - t0) / Vs
-    Vs = int(min(V_total, max(min_genes, target_s / max(per_gene, 1e-9))))
-    Vs = (Vs // 1024) * 1024 or min_genes
-    r, mu, D = philox.generate(SEED, Vs, N, K, Lam, rho)
-    state = {"st": ocavi.init(r, mu, D, hp)}
-
-    def sweep():
-        t = time.perf_counter()
-        nw = ocavi.step(state["st"], r, mu, D, hp)
-        ocavi.elbo(nw, r, mu, D, hp)
-        state["st"] = nw
-        return time.perf_counter() - t
-
-    sample = (f"first {Vs} genes of the seed-{SEED} N={N} dataset; one vb_step+vb_elbo of the reference "
-              f"algorithm (numpy oracle port of tissuemix.vb, 1024-gene chunks, 1 thread) per step, "
-              f"scaled by {V_total}/{Vs}")
-    return sweep, Vs, sample
-
-
-def _cpu_worker(args):
-    """One worker process: its own gene slice, barrier-started sweeps (see cpu_reference_parallel)."""
-    V_slice, N, steps, barrier, out = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    from oracle import cavi as ocavi
-    from oracle import philox
-
-    K, Lam, rho = truth(N)
-    r, mu, D = philox.generate(SEED, V_slice, N, K, Lam, rho)
-    hp = ocavi.default_hyper(N)
-    st = ocavi.init(r, mu, D, hp)
-    st = ocavi.step(st, r, mu, D, hp)  # warm-up
     barrier.wait()
-    for _ in range(steps):
+    for _ in range(n_steps):
         nw = ocavi.step(st, r, mu, D, hp)
         ocavi.elbo(nw, r, mu, D, hp)
         st = nw
-    barrier.wait()
-    out.put(0)
+        barrier.wait()
+    q.put(0)
 
 
-def cpu_reference_parallel(V_total, N, procs=None, steps=2, target_s=2.0):
-    """The reference algorithm on every host core: `procs` processes each sweep a 1/procs
-    slice of a bounded sample (the work of one sweep is a sum over genes), started
-    together; seconds per full-V sweep = wall per sweep x V_total / sample."""
+def cpu_reference(V_total, N, warmup, steps, budget_s, procs=None):
+    """The reference's algorithm on every host core, one process per core (its own thread pool
+    is slower than serial), each sweeping a contiguous slice of the dataset's
+    first V_s genes; V_s = V_total unless (warmup + steps) full sweeps would exceed budget_s or
+    40% of the host's free memory.  Every step is barrier-delimited; returns the mean wall
+    time of the `steps` timed sweeps and V_s (full-V sweeps/s = V_s / V_total / wall)."""
     import multiprocessing as mp
 
+    from oracle import cavi as ocavi
+    from oracle import philox
+
     procs = procs or os.cpu_count() or 1
-    sweep, Vs1, _ = cpu_reference_sample(V_total, N, target_s=target_s / 2)
-    per_gene = statistics.median([sweep() for _ in range(2)]) / Vs1
-    V_slice = max(1024, int(target_s / per_gene / 1024) * 1024)
+    K, Lam, rho = truth(N)
+    Vp = 20480  # probe: per-gene cost of one sweep on one core
+    r, mu, D = philox.generate(SEED, Vp, N, K, Lam, rho)
+    hp = ocavi.default_hyper(N)
+    st = ocavi.step(ocavi.init(r, mu, D, hp), r, mu, D, hp)
+    t0 = time.perf_counter()
+    ocavi.elbo(ocavi.step(st, r, mu, D, hp), r, mu, D, hp)
+    per_gene = (time.perf_counter() - t0) / Vp
+    unit = procs * 4096
+    by_time = budget_s / max(1, warmup + steps) * procs / per_gene
+    d = N - 1
+    by_mem = 0.4 * _mem_available() / (12.0 * (2 * (2 * d * d + 2 * d) + 2 + d))  # two states + data, x1.5
+    Vs = int(min(V_total, by_time, by_mem))
+    Vs = V_total if Vs >= V_total else max(unit, Vs // unit * unit)
+    bounds = [min(Vs, (Vs * k // procs) // 2 * 2) for k in range(procs + 1)]
+    bounds[-1] = Vs
     ctx = mp.get_context("fork")
     barrier = ctx.Barrier(procs + 1)
     q = ctx.Queue()
-    ps = [ctx.Process(target=_cpu_worker, args=((V_slice, N, steps, barrier, q),)) for _ in range(procs)]
+    n_steps = warmup + steps
+    ps = [ctx.Process(target=_ref_worker, args=((bounds[k], bounds[k + 1], V_total, N, n_steps, barrier, q),))
+          for k in range(procs)]
     for p_ in ps:
         p_.start()
-    barrier.wait()
-    t0 = time.perf_counter()
-    barrier.wait()
-    wall = (time.perf_counter() - t0) / steps
+    barrier.wait()  # every slice generated and initialised
+    marks = [time.perf_counter()]
+    for _ in range(n_steps):
+        barrier.wait()
+        marks.append(time.perf_counter())
     for p_ in ps:
         q.get()
         p_.join()
-    Vs = V_slice * procs
-    sample = (f"{procs} processes x the first {V_slice} genes of the seed-{SEED} N={N} dataset; vb_step+vb_elbo "
-              f"of the reference algorithm (numpy oracle port of tissuemix.vb), {steps} sweeps started together, "
-              f"wall per sweep scaled by {V_total}/{Vs}; single core: {1.0 / (per_gene * V_total):.4g} sweeps/s")
-    return wall * V_total / Vs, procs, sample
+    wall = (marks[-1] - marks[warmup]) / steps
+    sample = (f"{'the whole dataset' if Vs == V_total else f'the first {Vs} of {V_total} genes'} split over "
+              f"{procs} processes (one per core); per step every process runs vb_step + vb_elbo of the "
+              f"reference algorithm (numpy oracle port of tissuemix.vb, 1024-gene chunks, 1 thread) on its "
+              f"slice, steps barrier-delimited; {warmup} warm-up + {steps} timed steps"
+              + ("" if Vs == V_total else f"; iters/s scaled by {Vs}/{V_total}")
+              + f"; single core: {1.0 / (per_gene * V_total):.4g} full sweeps/s")
+    return wall, Vs, procs, sample
 
 
 def run_reference(args):
@@ -218,21 +249,17 @@ def run_reference(args):
     if rank != 0:
         return 0
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    V = int(args.genes)
-    per = []
-    for _ in range(max(1, min(args.steps, 3))):
-        t, cores, sample = cpu_reference_parallel(V, args.networks)
-        per.append(t)
-    per_sweep_full = statistics.median(per)
-    value = 1.0 / per_sweep_full
+    V, N = int(args.genes), args.networks
+    wall, Vs, cores, sample = cpu_reference(V, N, args.warmup, args.steps, budget_s=150.0)
+    value = Vs / V / wall
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_sweep_full * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"CAVI sweep, V={V:.0e} genes, N={args.networks} networks (K={args.networks}), "
-                               f"fp64, reference algorithm on host cores (bounded sample)",
-                   "V": V, "N": args.networks},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "config": bench_config(V, N, args.storage, args.gpus),
+        "sample_genes_per_step": Vs,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -249,7 +276,8 @@ def run_ours(args):
     if world != 1 or args.gpus != 1 or args.force_dist:
         from paper_2401_10068_b200 import dist  # noqa: PLC0415
 
-        return dist.bench_main(args, METRIC, UNIT, clocks_cls=Clocks)
+        return dist.bench_main(args, METRIC, UNIT, clocks_cls=Clocks,
+                               config=bench_config(int(args.genes), args.networks, args.storage, world))
 
     dev = _lib.default_device()
     V, N = int(args.genes), args.networks
@@ -285,14 +313,9 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if args.storage == "f64" else "f64 (fp32 storage)", "data": "synthetic",
-        "config": {"workload": f"CAVI sweep (fused E-pass + on-device K/Lambda/rho tail + ELBO), V={V:.0e} genes, "
-                               f"N={N} networks (d={d}), {args.storage} storage, inputs resident in HBM",
-                   "V": V, "N": N, "seed": SEED, "storage": args.storage,
-                   "l2": (f"inputs ({bytes_sweep / 1e9:.2f} GB) larger than L2 (126 MB); no flush needed"
-                          if bytes_sweep > 126e6 else
-                          f"inputs ({bytes_sweep / 1e6:.0f} MB) L2-resident by design (evict-last): the "
-                          f"small-V latency regime, not an HBM measurement"),
-                   "generate_s": round(gen_s, 3), "parallelism": "single GPU"},
+        "config": bench_config(V, N, args.storage),
+        "step": "one fused E-pass over the HBM-resident stream + the on-device K/Lambda/rho tail with the bound",
+        "generate_s": round(gen_s, 3),
         "gpu_launches": int(nl.value),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_kind": peak_kind,
@@ -312,8 +335,9 @@ def run_ours(args):
         line["e2e"] = e2e(args, dd, hp)
     del dd
     if not (args.no_cpu or args.profile):
-        t, cores, sample = cpu_reference_parallel(V, N)
-        line["cpu_baseline"] = {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        wall, Vs, cores, sample = cpu_reference(V, N, warmup=1, steps=2, budget_s=30.0)
+        line["cpu_baseline"] = {"value": Vs / V / wall, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": sample, "cpu": cpu_model()}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -350,8 +374,11 @@ def e2e(args, dd, hp):
         gc.collect()
     wall = statistics.median(times)
     M = int(statistics.median(sweeps))
-    return {"value": M / wall, "unit": UNIT, "h2d_bytes_per_step": int(8 * V * (2 + d)),
-            "d2h_bytes_per_step": int(C.sizeof(_lib.CvState) + 4 * 8 * M), "sweeps_per_call": M,
+    h2d, d2h = int(8 * V * (2 + d)), int(C.sizeof(_lib.CvState) + 4 * 8 * M)
+    return {"value": M / wall, "unit": UNIT, "h2d_bytes_per_step": h2d // M, "d2h_bytes_per_step": d2h // M,
+            "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h, "sweeps_per_call": M,
+            "step": "one sweep; a call = H2D of r, mu, D + vb_init + the sweeps to the stop rule + D2H of the "
+                    "state and trace, so the per-step bytes are the call's bytes / sweeps_per_call",
             "call": "paper_2401_10068_b200.vb.vb_fit(Dataset(host, pinned), hp" + (
                 ")  [reference defaults: max_iter=300, rel_tol=1e-8]" if not kw else f", max_iter={M}, rel_tol=0)"),
             "wall_s": wall}

@@ -116,7 +116,9 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
  * is copied to HBM and parsed there (one thread per line, Python float() syntax, correctly
  * rounded) straight into the dataset's stream layout.  Errors as the reference raises them
  * for the first offending row: CV_ERR_FORMAT (UsageError: header, field count) or
- * CV_ERR_ARG (ValueError: unparsable / non-finite value, no records). */
+ * CV_ERR_ARG (ValueError: unparsable / non-finite value, no records).  A file holding any
+ * quote character is read on the host with csv.reader's quoting rules instead (a field may
+ * then contain commas and line breaks), with the same checks and messages. */
 int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, cv_dataset** out,
                             int32_t* n_networks);
 /* cli.write_dataset_csv (cli.py:47-56): header r,d_1..d_N, rows repr(r), untransformed profile
@@ -127,6 +129,11 @@ int32_t cv_write_dataset_csv(const char* path, const double* r, const double* mu
  * (0 ok, 1 syntax error, 2 needs strtod; repr returns the length written, <= 32 chars) */
 int32_t cv_parse_number_host(const char* s, int64_t n, double* out);
 int32_t cv_format_repr(double x, char* out);
+/* test hook: the host csv.reader restatement that files containing a quote character take
+ * (quoted fields may span commas and lines): records of text[0..n) serialised into out as
+ * 0x1d + fields separated by 0x1f (nothing for the empty record []), each record ended by
+ * 0x1e; *used = bytes written (CV_ERR_ARG if cap is too small). */
+int32_t cv_csv_records_host(const char* text, int64_t n, char* out, int64_t cap, int64_t* used);
 
 /* Copy back x = r - mu, r, mu and D (row-major) of the shard; any pointer may be
  * NULL (r and mu exist for datasets made by create/generate/load_csv, which keep them). */

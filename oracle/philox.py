@@ -236,6 +236,29 @@ def generate(seed: int, V: int, N: int, K, Lam, rho: float, include_constant: bo
     return r, mu, D
 
 
+def generate_slice(seed: int, lo: int, hi: int, V_total: int, N: int, K, Lam, rho: float):
+    """Genes [lo, hi) of generate(seed, V_total, N, K, Lam, rho) without drawing the rest of
+    the stream (include_constant=True, where every uniform is one gene): the stream is
+    uniforms(V_total), normals(V_total d), normals(V_total) (model.py:224-270), each draw
+    block holding two values, so a slice starting at an even gene (lo d even) begins on a
+    block boundary of all three segments."""
+    if lo % 2 or hi < lo or hi > V_total:
+        raise ValueError("slice must start at an even gene inside the dataset")
+    K = np.atleast_1d(np.asarray(K, dtype=np.float64))
+    d = N - 1
+    n = hi - lo
+    b_z = -(-V_total // 2)
+    b_e = b_z + -(-(V_total * d) // 2)
+    codes = np.minimum((Stream(seed, block=lo // 2).uniforms(n) * 2 ** N).astype(np.int64), 2 ** N - 1)
+    mu, D = codes_to_working(codes, N)
+    L = chol_lower(inv_small(np.atleast_2d(Lam)))
+    z = Stream(seed, block=b_z + lo * d // 2).normals(n * d).reshape(n, d)
+    beta = K + z @ L.T
+    eps = Stream(seed, block=b_e + lo // 2).normals(n) / np.sqrt(rho)
+    r = np.einsum("vd,vd->v", D, beta) + mu + eps
+    return r, mu, D
+
+
 def make_regime(V: int, seed: int = 0, N: int = 3, K=None, rho: float = 100.0, include_constant=True):
     """The reference test-suite regime (reference tests/conftest.py:15-26).
 

@@ -97,6 +97,7 @@ _SIGS = {
     "cv_write_dataset_csv": (C.c_int32, [C.c_char_p, _D, _D, _D, C.c_int64, C.c_int32, C.c_int32]),
     "cv_parse_number_host": (C.c_int32, [C.c_char_p, C.c_int64, _D]),
     "cv_format_repr": (C.c_int32, [C.c_double, C.c_char_p]),
+    "cv_csv_records_host": (C.c_int32, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, _P(C.c_int64)]),
     "cv_kde_columns": (C.c_int32, [_D, C.c_int64, C.c_int32, _D, C.c_double, C.c_double, C.c_double, C.c_int32, _D,
                                    C.c_double, C.c_double, C.c_int32, C.c_int32, _D, _D]),
     "cv_kde_density": (C.c_int32, [_D, C.c_int64, C.c_double, C.c_double, _D, C.c_int64, C.c_int32, _D]),

@@ -545,6 +545,36 @@ int ensure_graph(cv_dataset* ds, int unroll) {
   return CV_OK;
 }
 
+// The sweep loop of cv_fit / cv_em_fit: CUDA graphs of `unroll` unrolled sweeps (every
+// kernel exits at its first instruction once the device's stop rule has set ctl->done), with
+// two groups in flight: group k+1 is queued before the host reads group k's done flag, so
+// the device never idles on the host round trip.  Returns once the stop rule fired or
+// `need` sweeps were queued.  After the stop rule fires, the one speculative group's
+// kernels all exit at once; groups are 16 sweeps at V > 4M genes (a group is >= 8 ms there)
+// and 32 below (0.3-0.6 ms of sweeps against ~70 us of empty launches after the stop).
+int run_groups(cv_dataset* ds, int need) {
+  const int unroll = need < 16 ? need : (ds->V > (1 << 22) ? 16 : 32);
+  int rc = ensure_graph(ds, unroll);
+  if (rc) return rc;
+  int launched = 0;
+  auto enqueue = [&](int b) -> int {
+    CK(cudaGraphLaunch(ds->graph, ds->stream));
+    launched += unroll;
+    CK(cudaMemcpyAsync(&ds->h_done[b], &ds->ctl->done, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaEventRecord(ds->ev[2 + b], ds->stream));
+    return CV_OK;
+  };
+  if ((rc = enqueue(0))) return rc;
+  for (int k = 0;; ++k) {
+    const int b = k & 1;
+    const bool more = launched < need;
+    if (more && (rc = enqueue(1 - b))) return rc;
+    CK(cudaEventSynchronize(ds->ev[2 + b]));
+    if (ds->h_done[b] || !more) break;
+  }
+  return CV_OK;
+}
+
 template <typename T>
 int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, const double* D) {
   // stage the host arrays in HBM, then transform into the SoA stream
@@ -889,8 +919,7 @@ double slow_value(const std::string& f) {
 }
 
 // one row on the host, same rules as row_parse_kernel; -1 when valid
-int host_row(const std::string& line, int N, double* v) {
-  const auto f = split_fields(line);
+int host_fields(const std::vector<std::string>& f, int N, double* v) {
   if ((int)f.size() != N + 1) return ingest::kErrFields;
   int bad_r = 0, bad_d = 0;
   for (int k = 0; k <= N; ++k) {
@@ -905,6 +934,111 @@ int host_row(const std::string& line, int N, double* v) {
   if (!std::isfinite(v[0])) return ingest::kErrNonfiniteR;
   return -1;
 }
+int host_row(const std::string& line, int N, double* v) { return host_fields(split_fields(line), N, v); }
+
+// Python's csv.reader (dialect "excel", strict=False) over a file opened with newline=''
+// (reference cli.py:58-60): the state machine of CPython's _csv.c (parse_process_char), fed
+// line by line as the io layer splits lines (\n, \r\n, lone \r) with an end-of-line event
+// after each.  Used for files that contain a quote character (quoted fields may hold commas,
+// doubled quotes and line breaks); quote-free files take the GPU path, whose line/field split
+// is this machine's behaviour on quote-free text.
+struct PyCsvReader {
+  enum { kEol = -2 };
+  enum St { START_RECORD, START_FIELD, IN_FIELD, IN_QUOTED_FIELD, QUOTE_IN_QUOTED_FIELD, EAT_CRNL };
+  const std::string& t;
+  size_t i = 0;
+  St st = START_RECORD;
+  std::string field;
+  std::vector<std::string>* row = nullptr;
+  bool bad = false;
+  explicit PyCsvReader(const std::string& text) : t(text) {}
+  void save() {
+    row->push_back(field);
+    field.clear();
+  }
+  void put(int c) {
+    switch (st) {
+      case START_RECORD:
+        if (c == kEol) return;  // an empty line: the record []
+        if (c == '\n' || c == '\r') {
+          st = EAT_CRNL;
+          return;
+        }
+        st = START_FIELD;
+        [[fallthrough]];
+      case START_FIELD:
+        if (c == '\n' || c == '\r' || c == kEol) {
+          save();
+          st = c == kEol ? START_RECORD : EAT_CRNL;
+        } else if (c == '"') {
+          st = IN_QUOTED_FIELD;
+        } else if (c == ',') {
+          save();
+        } else {
+          field.push_back((char)c);
+          st = IN_FIELD;
+        }
+        return;
+      case IN_FIELD:
+        if (c == '\n' || c == '\r' || c == kEol) {
+          save();
+          st = c == kEol ? START_RECORD : EAT_CRNL;
+        } else if (c == ',') {
+          save();
+          st = START_FIELD;
+        } else {
+          field.push_back((char)c);
+        }
+        return;
+      case IN_QUOTED_FIELD:
+        if (c == kEol) return;  // the record continues on the next line
+        if (c == '"') st = QUOTE_IN_QUOTED_FIELD;
+        else field.push_back((char)c);
+        return;
+      case QUOTE_IN_QUOTED_FIELD:
+        if (c == '"') {  // doubled quote
+          field.push_back('"');
+          st = IN_QUOTED_FIELD;
+        } else if (c == ',') {
+          save();
+          st = START_FIELD;
+        } else if (c == '\n' || c == '\r' || c == kEol) {
+          save();
+          st = c == kEol ? START_RECORD : EAT_CRNL;
+        } else {  // not strict: the character after the closing quote is kept
+          field.push_back((char)c);
+          st = IN_FIELD;
+        }
+        return;
+      case EAT_CRNL:
+        if (c == '\n' || c == '\r') return;
+        if (c == kEol) st = START_RECORD;
+        else bad = true;  // "new-line character seen in unquoted field" (unreachable with newline='')
+        return;
+    }
+  }
+  // the next record into `out`; false at the end of the input
+  bool next(std::vector<std::string>* out) {
+    out->clear();
+    row = out;
+    field.clear();
+    st = START_RECORD;
+    while (i < t.size()) {
+      size_t j = i;
+      while (j < t.size() && t[j] != '\n' && t[j] != '\r') ++j;
+      if (j < t.size()) j += (t[j] == '\r' && j + 1 < t.size() && t[j + 1] == '\n') ? 2 : 1;
+      for (size_t k = i; k < j; ++k) put((unsigned char)t[k]);
+      put(kEol);
+      i = j;
+      if (st == START_RECORD) return true;
+    }
+    if (!field.empty() || st == IN_QUOTED_FIELD) {  // end of data inside a field (not strict)
+      save();
+      return true;
+    }
+    return false;
+  }
+};
 
 int fetch_line(const char* dtext, const int64_t* dterm, int64_t l, std::string* out) {
   int64_t t2[2] = {-1, 0};
@@ -917,11 +1051,36 @@ int fetch_line(const char* dtext, const int64_t* dterm, int64_t l, std::string* 
   return CV_OK;
 }
 
-std::string py_str_repr(const std::string& s) { return "'" + s + "'"; }
+// repr() of a str (ASCII escapes as CPython's unicode_repr: the quote it picks, \\, \t \n \r,
+// \xNN for other control characters; non-ASCII bytes pass through)
+std::string py_str_repr(const std::string& s) {
+  const bool dq = s.find('\'') != std::string::npos && s.find('"') == std::string::npos;
+  const char q = dq ? '"' : '\'';
+  std::string o(1, q);
+  for (unsigned char c : s) {
+    if (c == (unsigned char)q || c == '\\') {
+      o.push_back('\\');
+      o.push_back((char)c);
+    } else if (c == '\t') {
+      o += "\\t";
+    } else if (c == '\n') {
+      o += "\\n";
+    } else if (c == '\r') {
+      o += "\\r";
+    } else if (c < 0x20 || c == 0x7f) {
+      char b[8];
+      snprintf(b, sizeof b, "\\x%02x", c);
+      o += b;
+    } else {
+      o.push_back((char)c);
+    }
+  }
+  o.push_back(q);
+  return o;
+}
 
 // the reference's message for the first bad row (cli.py:67-73, model.py:64-86)
-int row_error(const char* path, const std::string& line, int N, int kind) {
-  const auto f = split_fields(line);
+int row_error_fields(const char* path, const std::vector<std::string>& f, int N, int kind) {
   switch (kind) {
     case ingest::kErrFields:
       return fail(CV_ERR_FORMAT, "%s: row has %d fields, expected %d", path, (int)f.size(), N + 1);
@@ -938,6 +1097,9 @@ int row_error(const char* path, const std::string& line, int N, int kind) {
     default:
       return fail(CV_ERR_ARG, "expression reading must be finite");
   }
+}
+int row_error(const char* path, const std::string& line, int N, int kind) {
+  return row_error_fields(path, split_fields(line), N, kind);
 }
 
 struct LoadScratch {
@@ -1002,6 +1164,68 @@ int put_row(cv_dataset* ds, int64_t row, const double* v, int N) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+// A dataset file with quote characters: csv.reader semantics on the host (PyCsvReader), the
+// same per-row checks and messages as the device reader, then the upload path of
+// cv_dataset_create.  The reference writer never quotes, so this is the rare path.
+int load_csv_quoted(const char* path, int fd, int64_t size, int32_t storage, int32_t device, cv_dataset** out,
+                    int32_t* n_networks) {
+  std::string text((size_t)size, '\0');
+  for (int64_t got = 0; got < size;) {
+    const ssize_t m = pread(fd, &text[(size_t)got], (size_t)(size - got), got);
+    if (m <= 0) return fail(CV_ERR_ARG, "%s: short read", path);
+    got += m;
+  }
+  PyCsvReader rd(text);
+  std::vector<std::string> row;
+  if (!rd.next(&row) || row.empty() || row[0] != "r" || row.size() < 3)
+    return fail(CV_ERR_FORMAT, "%s: expected header r,d_1,...,d_N", path);
+  const int N = (int)row.size() - 1;
+  const int d = N - 1;
+  if (d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
+  std::vector<double> r, mu, D;
+  double v[ingest::kMaxFields];
+  while (rd.next(&row)) {
+    if (row.empty()) continue;
+    const int kind = host_fields(row, N, v);
+    if (kind >= 0) return row_error_fields(path, row, N, kind);
+    r.push_back(v[0]);
+    mu.push_back(v[N]);
+    for (int j = 0; j < d; ++j) D.push_back(v[1 + j] - v[N]);
+  }
+  if (r.empty()) return fail(CV_ERR_ARG, "no records");
+  const int rc = cv_dataset_create(r.data(), mu.data(), D.data(), (int64_t)r.size(), d, 0, (int64_t)r.size(), storage,
+                                   device, out);
+  if (rc == CV_OK && n_networks) *n_networks = N;
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t cv_csv_records_host(const char* text, int64_t n, char* out, int64_t cap, int64_t* used) {
+  if (!text || !out || !used || n < 0) return fail(CV_ERR_ARG, "null pointer");
+  const std::string t(text, (size_t)n);
+  PyCsvReader rd(t);
+  std::vector<std::string> row;
+  std::string o;
+  while (rd.next(&row)) {
+    if (!row.empty()) o.push_back('\x1d');  // distinguishes [''] from []
+    for (size_t k = 0; k < row.size(); ++k) {
+      if (k) o.push_back('\x1f');
+      o += row[k];
+    }
+    o.push_back('\x1e');
+  }
+  *used = (int64_t)o.size();
+  if ((int64_t)o.size() > cap) return fail(CV_ERR_ARG, "output buffer too small");
+  std::memcpy(out, o.data(), o.size());
+  return CV_OK;
+}
+
 int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, cv_dataset** out,
                             int32_t* n_networks) {
   if (!path || !out) return fail(CV_ERR_ARG, "null pointer");
@@ -1034,6 +1258,7 @@ int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, c
       if (!done) off += n;
     }
   }
+  if (head.find('"') != std::string::npos) return load_csv_quoted(path, sc.fd, size, storage, device, out, n_networks);
   const auto hf = split_fields(head);
   if (size == 0 || head.empty() || hf[0] != "r" || hf.size() < 3)
     return fail(CV_ERR_FORMAT, "%s: expected header r,d_1,...,d_N", path);
@@ -1075,6 +1300,17 @@ int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, c
   if (last != '\n' && last != '\r') {  // the final line has no terminator: give it one
     CK(cudaMemsetAsync(dtext + S0, '\n', 1, sc.st));
     S = S0 + 1;
+  }
+  {  // any quote character: csv.reader's quoting spans fields and lines -> the host reader
+    int* dq = nullptr;
+    CK(sc.alloc(&dq, sizeof(int)));
+    CK(cudaMemsetAsync(dq, 0, sizeof(int), sc.st));
+    ingest::quote_any_kernel<<<(unsigned)std::min<int64_t>(tiles, 1184), 256, 0, sc.st>>>(dtext, S, dq);
+    CK(cudaGetLastError());
+    int hq = 0;
+    CK(cudaMemcpyAsync(&hq, dq, sizeof(int), cudaMemcpyDeviceToHost, sc.st));
+    CK(cudaStreamSynchronize(sc.st));
+    if (hq) return load_csv_quoted(path, sc.fd, size, storage, device, out, n_networks);
   }
   // 1. line terminators
   int64_t *tcount = nullptr, *tbase = nullptr;
@@ -1270,28 +1506,7 @@ int32_t cv_fit(cv_dataset* ds, const cv_hyper* hp, int32_t max_iter, double rel_
   init_gen_kernel<<<1, 1, 0, ds->stream>>>(ds->hyp, ds->ctl);
   CK(cudaGetLastError());
   if ((rc = launch_pass(ds))) return rc;
-  // sweeps: unrolled graphs; every pass kernel exits at once after the stop rule fired
-  const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
-  if ((rc = ensure_graph(ds, unroll))) return rc;
-  // Two groups in flight: group k+1 is queued before the host reads group k's done flag,
-  // so the device never idles on the host round trip.  After the stop rule fires, the one
-  // extra group's kernels all exit at once (they read ctl->done first).
-  int launched = 0;
-  auto enqueue = [&](int b) -> int {
-    CK(cudaGraphLaunch(ds->graph, ds->stream));
-    launched += unroll;
-    CK(cudaMemcpyAsync(&ds->h_done[b], &ds->ctl->done, sizeof(int), cudaMemcpyDeviceToHost, ds->stream));
-    CK(cudaEventRecord(ds->ev[2 + b], ds->stream));
-    return CV_OK;
-  };
-  if ((rc = enqueue(0))) return rc;
-  for (int k = 0;; ++k) {
-    const int b = k & 1;
-    const bool more = launched < max_iter;
-    if (more && (rc = enqueue(1 - b))) return rc;
-    CK(cudaEventSynchronize(ds->ev[2 + b]));
-    if (ds->h_done[b] || !more) break;
-  }
+  if ((rc = run_groups(ds, max_iter))) return rc;
   if ((rc = ctl_get(ds))) return rc;  // stream-ordered after the extra group
   const Ctl& h = *ds->h_ctl;
   *out = h.cur;
@@ -1348,15 +1563,7 @@ int32_t cv_em_fit(cv_dataset* ds, const double* K, const double* Lam, double rho
   int rc = em_setup(ds, K, Lam, rho, max_iter, rel_tol, max_iter, c);
   if (rc) return rc;
   if ((rc = launch_pass(ds))) return rc;  // pass 0: ll(theta_0) + M-step
-  const int unroll = max_iter < 16 ? max_iter : (ds->V > (1 << 22) ? 16 : 64);
-  if ((rc = ensure_graph(ds, unroll))) return rc;
-  for (int launched = 0;;) {
-    CK(cudaMemcpyAsync(&ds->h_ctl->done, &ds->ctl->done, sizeof(int) * 4, cudaMemcpyDeviceToHost, ds->stream));
-    CK(cudaStreamSynchronize(ds->stream));
-    if (ds->h_ctl->done || launched > max_iter) break;
-    CK(cudaGraphLaunch(ds->graph, ds->stream));
-    launched += unroll;
-  }
+  if ((rc = run_groups(ds, max_iter + 1))) return rc;  // pass n: ll(theta_n) + M-step, n <= max_iter
   if ((rc = ctl_get(ds))) return rc;
   const Ctl& h = *ds->h_ctl;
   if (h.status != CV_OK) return fail(h.status, h.status == CV_ERR_NUMERIC ? "EM step failed: non-positive residual "

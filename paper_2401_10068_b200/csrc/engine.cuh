@@ -4,15 +4,14 @@
 // A sweep = one fused streaming pass over the measurements (pass.cuh) that
 // yields the per-sweep statistic vector
 //     [ g (d) | G upper triangle (d(d+1)/2) | R | Ld ]
-// followed by this tail, run by the last CTA of the pass (single GPU) or by a
-// one-CTA kernel after the NCCL exchange (multi-GPU).  The tail restates
+// followed by this tail, run by a separate one-warp kernel (pass.cuh tail_kernel) after
+// the pass (and, on several GPUs, after the exchange).  The tail restates
 // reference vb.py:136-197 (the rho and (K, Lambda) blocks) and vb.py:216-304
 // (the bound) in the centred rank-1 form of SURVEY Appendix A, and the fit
 // loop's bookkeeping and stop rule (vb.py:307-347).
 //
-// The tail is templated on d and works in registers / the thread's stack and
-// in place on the control block: it sits on the critical path of every sweep
-// (a single thread runs it after the last chunk), so it must cost
+// The tail is templated on d and works in registers and in place on the control
+// block: it sits on the critical path of every sweep, so it must cost
 // microseconds, not a walk through global-memory scratch.
 #pragma once
 
@@ -29,8 +28,6 @@ constexpr int kMaxStats = kMaxD + kMaxD * (kMaxD + 1) / 2 + 3;  // 138
 constexpr int kChunk = 4096;         // genes per chunk (one reduction unit)
 constexpr int kGroupChunks = 64;     // chunks per group
 constexpr int kOctants = 8;          // top of the reduction tree (GPU-count invariant)
-constexpr int kThreads = 256;        // consumer threads per CTA of the pass
-constexpr int kWarps = kThreads / 32;
 
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr double kLnPi = 1.14472988584940017414;

@@ -36,6 +36,25 @@ enum : int {
   kErrNonfiniteR = 4,  // RawRecord: expression reading must be finite
 };
 
+// any '"' in the body: such files go to the host reader (csv.reader's quoting rules span
+// commas and line breaks, which the line-parallel split cannot see)
+static __global__ void quote_any_kernel(const char* t, int64_t n, int* flag) {
+  const int64_t n16 = n / 16;
+  int hit = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(t)[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // SWAR: a zero byte of w ^ 0x22222222 is a quote
+      const uint32_t x = w[k] ^ 0x22222222u;
+      hit |= ((x - 0x01010101u) & ~x & 0x80808080u) != 0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int64_t i = n16 * 16; i < n; ++i) hit |= t[i] == '"';
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 __device__ __forceinline__ bool is_term(const char* t, int64_t n, int64_t i) {
   const char c = t[i];
   return c == '\n' || (c == '\r' && (i + 1 >= n || t[i + 1] != '\n'));

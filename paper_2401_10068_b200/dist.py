@@ -185,7 +185,7 @@ def fit_many_partitioned(datasets, hp, rank: int | None = None, world: int | Non
 
 
 # ---------------------------------------------------------------------------- bench leg
-def bench_main(args, metric: str, unit: str, clocks_cls=None) -> int:
+def bench_main(args, metric: str, unit: str, clocks_cls=None, config=None) -> int:
     """bench.py at N>1: strong scaling of the V-gene sweep over the ranks of torchrun.
 
     Device-timed sweeps (max over ranks), nvidia-smi clocks during them (rank 0's GPU),
@@ -249,12 +249,10 @@ def bench_main(args, metric: str, unit: str, clocks_cls=None) -> int:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if args.storage == "f64" else "f64 (fp32 storage)",
             "data": "synthetic",
-            "config": {"workload": f"CAVI sweep, V={V:.0e} genes sharded by octant over {world} GPUs, N={N} "
-                                   f"(d={d}), {args.storage} storage, per-sweep exchange of {ns} doubles: "
-                                   + ("fused into the pass (NVLink stores into NCCL symmetric windows)"
-                                      if comm.fused else "one ncclAllGather"),
-                       "V": V, "N": N, "parallelism": f"dp{world} (gene shards)",
-                       "l2": "per-rank stream larger than L2"},
+            "config": config or {"V": V, "N": N, "parallelism": f"dp{world} (gene shards)"},
+            "exchange": f"per-sweep exchange of {ns} doubles: " + (
+                "fused into the pass (NVLink stores into NCCL symmetric windows)" if comm.fused
+                else "one ncclAllGather"),
             "gpu_launches": int(nl.value),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "per": "largest rank shard, max over ranks"},
@@ -304,8 +302,9 @@ def _e2e_sharded(args, shard, comm, td, hp, unit):
         gc.collect()
     wall = statistics.median(times)
     M = int(statistics.median(sweeps))
-    return {"value": M / wall, "unit": unit, "h2d_bytes_per_step": int(8 * shard.V_total * (2 + d)),
-            "d2h_bytes_per_step": int(comm.world * (C.sizeof(_lib.CvState) + 4 * 8 * M)), "sweeps_per_call": M,
+    h2d, d2h = int(8 * shard.V_total * (2 + d)), int(comm.world * (C.sizeof(_lib.CvState) + 4 * 8 * M))
+    return {"value": M / wall, "unit": unit, "h2d_bytes_per_step": h2d // M, "d2h_bytes_per_step": d2h // M,
+            "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h, "sweeps_per_call": M,
             "call": "per rank: dist.shard_upload(Dataset(host shard, pinned)) + vb.vb_fit(shard, hp)"
                     + ("  [reference defaults]" if not kw else f", max_iter={M}, rel_tol=0"),
             "wall_s": wall}

@@ -43,12 +43,15 @@ def load_dataset_csv(path, storage: str = "f64", device: int | None = None) -> m
 
 
 def read_dataset_csv(path) -> model.Dataset:
-    """The reference's reader (cli.py:58-75): the working-transform Dataset on the host."""
+    """The reference's reader (cli.py:58-75): the working-transform Dataset on the host.  The
+    parsed HBM stream stays attached to it (vb.keep_resident), so the vb_fit that follows
+    (cli._fit_vb, cli.py:235-268) starts from it instead of uploading the arrays again."""
+    from . import vb  # noqa: PLC0415
+
     dd = load_dataset_csv(path)
-    try:
-        return dd.to_host()
-    finally:
-        dd.close()
+    ds = dd.to_host()
+    vb.keep_resident(ds, dd)
+    return ds
 
 
 def write_dataset_csv(path, ds, threads: int = 0) -> None:

@@ -47,7 +47,13 @@ def device_dataset(ds, storage: str = "f64") -> model.DeviceDataset:
     hit = _resident.get(key)
     if hit is not None and hit[0]() is ds:
         return hit[1]
-    dd = model.upload(ds, storage=storage)
+    return keep_resident(ds, model.upload(ds, storage=storage), storage)
+
+
+def keep_resident(ds, dd: model.DeviceDataset, storage: str = "f64") -> model.DeviceDataset:
+    """Register `dd` as the HBM copy of host dataset `ds` for the dataset's lifetime (e.g. the
+    stream the GPU reader parsed a file into, so the CLI's vb_fit does not upload it again)."""
+    key = (id(ds), storage)
     try:
         ref = weakref.ref(ds, lambda _r, k=key: _resident.pop(k, None))
     except TypeError:  # objects without weakref support: keep only the latest

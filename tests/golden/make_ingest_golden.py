@@ -62,6 +62,14 @@ def hand_files():
     f["err_bad_r_nan_d.csv"] = "r,d_1,d_2\n1..2,1,nan\n"
     f["err_underscore.csv"] = "r,d_1,d_2\n1__0,1,0\n"
     f["err_ws_only_row.csv"] = "r,d_1,d_2\n0.1,1,0\n   \n"
+    # csv.reader quoting (the GPU reader hands any file with a quote to the host reader)
+    f["quoted_fields.csv"] = ('"r","d_1","d_2"\n"0.5","1","0"\n"1.5",0,"1"\n"2.5\n",1,0\n'
+                              '"-1.25" ,1,0\n\n"3"e0,0,1\r\n4.5,"1","0"\r\n"7.0",1,"1\n"\n')
+    f["err_quoted_comma.csv"] = 'r,d_1,d_2\n0.1,1,0\n"1,5",1,0\n'
+    f["err_quoted_fields.csv"] = 'r,d_1,d_2\n0.1,"1,0"\n'
+    f["err_doubled_quote.csv"] = 'r,d_1,d_2\n"1""0",1,0\n'
+    f["err_quote_in_field.csv"] = "r,d_1,d_2\n0.5,1,0\n0.25,x'\"y,0\n"
+    f["err_quoted_header.csv"] = '"r,d_1",d_2\n0.1,1\n'
     return f
 
 

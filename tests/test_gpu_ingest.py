@@ -115,3 +115,16 @@ def test_awkward_text_is_parsed_like_python(ing, tmp_path):
     assert np.array_equal(bits(ds.r), bits(want[:, 0]))
     assert np.array_equal(bits(ds.mu), bits(want[:, 2]))
     assert np.array_equal(bits(ds.D[:, 0]), bits(want[:, 1] - want[:, 2]))
+
+
+def test_read_dataset_keeps_its_hbm_stream(ing):
+    """The CLI's read -> vb_fit path (cli.py:235-268 after install()) uploads nothing again:
+    the Dataset read_dataset_csv returns carries the stream the GPU reader parsed."""
+    from paper_2401_10068_b200 import vb
+
+    path = os.path.join(GOLD, "w_n8_2000.csv")
+    ds = ing.read_dataset_csv(path)
+    dd = vb.device_dataset(ds)
+    assert vb.device_dataset(ds) is dd and dd.V == ds.V
+    x = dd.stream_x()
+    assert np.array_equal(bits(x), bits(ds.r - ds.mu))

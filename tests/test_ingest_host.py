@@ -157,3 +157,36 @@ def test_header_errors_before_any_device_work(lib, name):
     with pytest.raises(ingest.UsageError) as info:
         ingest.load_dataset_csv(path, device=0)
     assert str(info.value) == e["message"].replace("{path}", path)
+
+
+def _records(text):
+    import ctypes as C
+
+    from paper_2401_10068_b200 import _lib
+
+    b = text.encode("latin-1")
+    out, used = C.create_string_buffer(4 * len(b) + 64), C.c_int64()
+    _lib.check(_lib.lib().cv_csv_records_host(b, len(b), out, len(out), C.byref(used)))
+    s = out.raw[: used.value].decode("latin-1")
+    return [rec[1:].split("\x1f") if rec.startswith("\x1d") else [] for rec in s.split("\x1e")[:-1]]
+
+
+def test_host_csv_reader_is_pythons_csv_reader():
+    """Files with a quote character are read on the host by a restatement of csv.reader
+    (dialect excel, newline='', reference cli.py:58-60); fuzzed against the real module."""
+    import csv
+    import io
+    import random
+
+    rng = random.Random(1)
+    alpha = ["a", "1", ",", '"', "\n", "\r", " ", "\r\n", '""', "2.5"]
+    checked = 0
+    for _ in range(20000):
+        t = "".join(rng.choice(alpha) for _ in range(rng.randint(0, 16)))
+        try:
+            want = list(csv.reader(io.StringIO(t, newline="")))
+        except csv.Error:
+            continue
+        assert _records(t) == want, repr(t)
+        checked += 1
+    assert checked > 15000
