@@ -182,6 +182,17 @@ struct CallScratch {
   }
 };
 
+// octants of this shard that hold groups
+void count_live_octants(cv_dataset* ds) {
+  ds->n_live_octants = 0;
+  for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
+    const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
+    const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
+                                         ds->group_lo + ds->n_groups);
+    if (h1 > h0) ++ds->n_live_octants;
+  }
+}
+
 #define PALLOC(ptr, bytes) CK(pool_alloc((void**)&(ptr), (bytes), ds->stream, ds->device))
 
 int plan_and_alloc(cv_dataset* ds) {
@@ -228,13 +239,7 @@ int plan_and_alloc(cv_dataset* ds) {
   CK(cudaMemsetAsync(ds->ticket, 0, sizeof(unsigned long long), ds->stream));
   PALLOC(ds->opartials, sizeof(double) * ns * kOctants);
   PALLOC(ds->tot, sizeof(double) * kMaxStats * kOctants);
-  ds->n_live_octants = 0;
-  for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
-    const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
-    const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
-                                         ds->group_lo + ds->n_groups);
-    if (h1 > h0) ++ds->n_live_octants;
-  }
+  count_live_octants(ds);
   PALLOC(ds->flags, sizeof(int) * 4);
   CK(cudaMemsetAsync(ds->flags, 0, sizeof(int) * 4, ds->stream));
   PALLOC(ds->ctl, sizeof(Ctl));
@@ -673,13 +678,7 @@ int32_t cv_dataset_set_shard(cv_dataset* ds, int32_t rank, int32_t world) {
   if (ds->gene_lo + ds->V != want_hi && ds->V > 0) return fail(CV_ERR_ARG, "shard is not rank %d's octant span", rank);
   ds->oct_lo = rank * per;
   ds->oct_hi = ds->oct_lo + per;
-  ds->n_live_octants = 0;
-  for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
-    const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
-    const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
-                                         ds->group_lo + ds->n_groups);
-    if (h1 > h0) ++ds->n_live_octants;
-  }
+  count_live_octants(ds);
   if (ds->graph) {
     CK(cudaGraphExecDestroy(ds->graph));
     ds->graph = nullptr;
@@ -1873,19 +1872,33 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   if (rc) return rc;
   CK(cudaStreamSynchronize(ds->stream));
   if (const char* path = getenv("CAVI_TRACE_CTA")) {
-    // diagnostics: one more sweep with per-CTA globaltimer stamps, dumped as text
+    // diagnostics: 3 more PDL-chained sweeps; per-CTA globaltimer stamps of the last pass
+    // [resident pre-wait, post-wait start, producer end, consumer end, smid, cascade entry,
+    // final tree start, totals written] and the tails' entry / exit stamps, dumped as text
+    const int nt = 3;
+    unsigned long long* tl = nullptr;
     CK(cudaMalloc(&ds->cta_trace, sizeof(unsigned long long) * 8 * ds->grid));
+    CK(cudaMalloc(&tl, sizeof(unsigned long long) * 2 * nt));
     CK(cudaMemsetAsync(ds->cta_trace, 0, sizeof(unsigned long long) * 8 * ds->grid, ds->stream));
-    if ((rc = launch_pass(ds))) return rc;
-    std::vector<unsigned long long> tr(8 * (size_t)ds->grid);
+    CK(cudaMemsetAsync(tl, 0, sizeof(unsigned long long) * 2 * nt, ds->stream));
+    CK(cudaMemcpyAsync(&ds->ctl->tl_trace, &tl, sizeof tl, cudaMemcpyHostToDevice, ds->stream));
+    CK(cudaMemsetAsync(&ds->ctl->tl_n, 0, sizeof(int), ds->stream));
+    CK(cudaStreamSynchronize(ds->stream));
+    for (int i = 0; i < nt && rc == CV_OK; ++i) rc = launch_pass(ds);
+    if (rc) return rc;
+    std::vector<unsigned long long> tr(8 * (size_t)ds->grid), tt(2 * nt);
     CK(cudaMemcpyAsync(tr.data(), ds->cta_trace, sizeof(unsigned long long) * tr.size(), cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaMemcpyAsync(tt.data(), tl, sizeof(unsigned long long) * tt.size(), cudaMemcpyDeviceToHost, ds->stream));
+    CK(cudaMemsetAsync(&ds->ctl->tl_trace, 0, sizeof tl, ds->stream));
     CK(cudaStreamSynchronize(ds->stream));
     CK(cudaFree(ds->cta_trace));
+    CK(cudaFree(tl));
     ds->cta_trace = nullptr;
     if (FILE* f = fopen(path, "w")) {
+      for (int i = 0; i < nt; ++i) fprintf(f, "tail %d %llu %llu\n", i, tt[2 * i], tt[2 * i + 1]);
       for (int b = 0; b < ds->grid; ++b)
-        fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu\n", b, tr[8 * b], tr[8 * b + 1], tr[8 * b + 2], tr[8 * b + 3],
-                tr[8 * b + 4], tr[8 * b + 5], tr[8 * b + 6]);
+        fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu %llu\n", b, tr[8 * b + 7], tr[8 * b], tr[8 * b + 1],
+                tr[8 * b + 2], tr[8 * b + 3], tr[8 * b + 4], tr[8 * b + 5], tr[8 * b + 6]);
       fclose(f);
     }
   }
@@ -1903,9 +1916,10 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   if ((rc = ctl_get(ds))) return rc;
   if (getenv("CAVI_TAIL_PROF_PRINT")) {
     const unsigned long long* p = ds->h_ctl->prof;
-    fprintf(stderr, "tail cycles: combine %lld loads %lld update %lld elbo %lld bookkeeping %lld stores %lld\n",
-            (long long)(p[6] - p[0]), (long long)(p[1] - p[6]), (long long)(p[2] - p[1]), (long long)(p[3] - p[2]),
-            (long long)(p[4] - p[3]), (long long)(p[5] - p[4]));
+    fprintf(stderr,
+            "tail cycles: loads %lld products %lld update+inverse %lld elbo %lld deltas %lld stores %lld total %lld\n",
+            (long long)(p[1] - p[0]), (long long)(p[6] - p[1]), (long long)(p[2] - p[6]), (long long)(p[3] - p[2]),
+            (long long)(p[4] - p[3]), (long long)(p[5] - p[4]), (long long)(p[5] - p[0]));
   }
   if (ds->h_ctl->status != CV_OK) return state_status(ds->h_ctl->cur);
   return CV_OK;

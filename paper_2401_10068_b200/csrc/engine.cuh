@@ -95,6 +95,8 @@ struct Ctl {
   double* tr_k;  // EM: K per iteration [tr_cap][d]
   int tr_cap;
   unsigned long long prof[8];  // CAVI_TAIL_PROF builds: clock64 stamps of the last tail
+  unsigned long long* tl_trace;  // diagnostics (CAVI_TRACE_CTA): globaltimer at tail entry / exit, per sweep
+  int tl_n;
 };
 
 #ifdef CAVI_TAIL_PROF

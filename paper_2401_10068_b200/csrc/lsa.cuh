@@ -74,6 +74,20 @@ __device__ __forceinline__ void lsa_publish(const LsaLink& L, uint64_t s, int ns
   }
 }
 
+// One statistic of this rank for sequence s into every peer (the pass's final warp, lane-wise)
+__device__ __forceinline__ void lsa_publish_stat(const LsaLink& L, uint64_t s, int st, double v) {
+  if (L.seq[1] == s) return;  // injected fault: this rank never publishes sweep s
+  const int par = (int)(s & 1);
+  const uint64_t tag = (uint64_t)(uint32_t)s << 32;
+  const uint64_t u = (uint64_t)__double_as_longlong(v);
+  const uint64_t w0 = tag | (u & 0xffffffffull), w1 = tag | (u >> 32);
+  for (int p = 0; p < L.world; ++p) {
+    uint64_t* dst = static_cast<uint64_t*>(ncclGetLsaPointer(L.win, lsa_data_off(par, L.rank), p)) + 2 * st;
+    st_relaxed_sys(dst, w0);
+    st_relaxed_sys(dst + 1, w1);
+  }
+}
+
 // Value of statistic st from rank r for sequence s, polled from this rank's window
 // (bounded by the globaltimer deadline; *ok = false on timeout).
 __device__ __forceinline__ double lsa_take(const LsaLink& L, uint64_t s, int r, int st, unsigned long long deadline,

@@ -26,6 +26,7 @@
 #include "engine.cuh"
 #include "lsa.cuh"
 #include "ptx.cuh"
+#include "tail.cuh"
 
 namespace cavi {
 
@@ -266,10 +267,42 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
+// The plan's fixed-order row sum (as warp_sum_rows: lane l adds rows l, l+32, ... from 0.0 in
+// index order, then the 16-8-4-2-1 xor butterfly) with the result left in registers: lane l
+// gets stat l + 32k in out[k].
+template <int NS>
+__device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (&out)[(NS + 31) / 32], int lane) {
+  constexpr int B = NS < 16 ? NS : 16;
+#pragma unroll
+  for (int k = 0; k < (NS + 31) / 32; ++k) out[k] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < NS; s0 += B) {
+    double acc[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = 0.0;
+#pragma unroll 2
+    for (int64_t i = lane; i < n; i += 32) {
+      const double* row = src + i * NS + s0;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (s0 + b < NS) acc[b] += __ldcg(row + b);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      double v = acc[b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (s0 + b < NS && (s0 + b) % 32 == lane) out[(s0 + b) / 32] = v;
+    }
+  }
+}
+
 // chunk partial -> group -> octant -> total (-> tail), by whichever warp completes each level
+// (arrival counters: nobody waits for anybody).  The final level keeps the octant totals in
+// registers and issues every octant load at once (one L2 round trip for the tree).
 template <int D, int NS = n_stats(D)>
-__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, double* s_tot,
-                                          int lane) {
+__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, int lane) {
+  constexpr int K = (NS + 31) / 32;
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) a.partials[chunk * NS + st] = chunk_sum[st];
   const int64_t grp = chunk / kGroupChunks;
@@ -282,68 +315,95 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
   const int o = (int)(gg / a.groups_per_octant);
   const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
   const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
+  double osum[K];
   if (g1 - g0 == 1) {
     // a one-group octant: its sum over one row is the row itself (the butterfly adds zeros),
     // so the group completes the octant directly (small V: one arrival level less)
-    warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.opartials + o * NS, lane);
+    warp_rows<NS>(a.partials + c0 * NS, nc, osum, lane);
   } else {
-    warp_sum_rows<NS>(a.partials + c0 * NS, nc, a.gpartials + grp * NS, lane);
+    warp_rows<NS>(a.partials + c0 * NS, nc, osum, lane);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) a.gpartials[grp * NS + lane + 32 * k] = osum[k];
     if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
     // octant complete
     if (lane == 0) a.ocount[o] = 0u;
-    warp_sum_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, a.opartials + o * NS, lane);
+    warp_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, osum, lane);
   }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (lane + 32 * k < NS) a.opartials[o * NS + lane + 32 * k] = osum[k];
   if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
-  // every octant this shard owns is complete: pairwise tree over them (empty octants add 0)
+  // every octant this shard owns is complete: pairwise tree over them (empty octants add 0);
+  // this warp's own octant from registers, the others' loads all in flight together
   if (lane == 0) *a.odone = 0u;
   if (a.cta_trace && lane == 0) {
     a.cta_trace[blockIdx.x * 8 + 4] = t_entry;
     a.cta_trace[blockIdx.x * 8 + 5] = globaltimer_ns();
   }
-  auto total = [&](int st) {
+  double tot[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int st = lane + 32 * k;
     double v[kOctants];
 #pragma unroll
-    for (int q = 0; q < kOctants; ++q) v[q] = 0.0;
-    for (int q = a.oct_lo; q < a.oct_hi; ++q) {
+    for (int q = 0; q < kOctants; ++q) {
       const int64_t h0 = lmax((int64_t)q * a.groups_per_octant, a.group_lo);
       const int64_t h1 = lmin(lmin((int64_t)(q + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
-      if (h1 > h0) v[q] = __ldcg(a.opartials + q * NS + st);
+      const bool live = st < NS && q >= a.oct_lo && q < a.oct_hi && h1 > h0;
+      v[q] = q == o ? osum[k] : (live ? __ldcg(a.opartials + q * NS + st) : 0.0);
     }
-    for (int w = 1; w < a.oct_hi - a.oct_lo; w *= 2)
-      for (int q = a.oct_lo; q + w < a.oct_hi; q += 2 * w) v[q] = v[q] + v[q + w];
-    return v[a.oct_lo];
-  };
-  if (a.lsa.win) {  // fused exchange: straight into every peer's window over NVLink
-    lsa_publish(a.lsa, *a.lsa.seq + 1, NS, total, lane);
-  } else {
-    for (int st = lane; st < NS; st += 32) a.rank_out[st] = total(st);
+#pragma unroll
+    for (int w = 1; w < kOctants; w *= 2)
+#pragma unroll
+      for (int q = 0; q + w < kOctants; q += 2 * w)
+        if (q >= a.oct_lo && q + w < a.oct_hi && ((q - a.oct_lo) % (2 * w)) == 0) v[q] = v[q] + v[q + w];
+    tot[k] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kOctants; ++q)
+      if (q == a.oct_lo) tot[k] = v[q];
   }
-  (void)s_tot;
+  if (a.lsa.win) {  // fused exchange: straight into every peer's window over NVLink
+    const uint64_t sq = *a.lsa.seq + 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) lsa_publish_stat(a.lsa, sq, lane + 32 * k, tot[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) a.rank_out[lane + 32 * k] = tot[k];
+  }
   if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
 }
 
-// The sweep tail as its own one-warp kernel (full register file: the tail is a long
-// dependent scalar chain and must not spill): pairwise tree over the `world` shard
-// totals (1 on a single GPU; the NCCL-gathered rank partials otherwise), then tail_t.
+// The sweep tail as its own one-warp kernel (tail.cuh): pairwise tree over the `world` shard
+// totals (1 on a single GPU; the NCCL-gathered rank partials or the fused exchange's window
+// otherwise), then the warp-parallel tail.
 template <int D>
 __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, Ctl* c, const double* parts, int world,
                                                      LsaLink lsa) {
   constexpr int NS = n_stats(D);
-  __shared__ double tot[NS];
+  __shared__ TailSm<D> sm;
   ptx::griddep_launch_dependents();  // the next pass may launch and stage its prologue
   ptx::griddep_wait();               // the pass (or exchange) that produced `parts` is complete
   if (threadIdx.x == 0) TAIL_PROF(*c, 0);
-  if (*(volatile const int*)&c->done) return;
+  const unsigned long long t_entry = globaltimer_ns();  // diagnostics (stored at exit: no load on the critical path)
   if (lsa.win) {  // fused exchange: every rank's partial arrives in this rank's window
+    if (*(volatile const int*)&c->done) return;  // no rank published this sweep
     const uint64_t s = *lsa.seq + 1;
     const unsigned long long deadline = lsa_now_ns() + lsa.timeout_ns;  // a stalled peer -> error, not a hang
     bool ok = true;
     for (int st = threadIdx.x; st < NS; st += 32) {
       double v[kOctants];
-      for (int r = 0; r < world; ++r) v[r] = lsa_take(lsa, s, r, st, deadline, &ok);
-      for (int w = 1; w < world; w *= 2)
-        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
-      tot[st] = v[0];
+#pragma unroll
+      for (int r = 0; r < kOctants; ++r)
+        if (r < world) v[r] = lsa_take(lsa, s, r, st, deadline, &ok);
+#pragma unroll
+      for (int w = 1; w < kOctants; w *= 2)
+#pragma unroll
+        for (int r = 0; r + w < kOctants; r += 2 * w)
+          if (w < world && r + w < world) v[r] = v[r] + v[r + w];
+      sm.tot[st] = v[0];
     }
     if (!__all_sync(0xffffffffu, ok)) {
       if (threadIdx.x == 0) {
@@ -354,88 +414,18 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
     }
     __syncwarp();
     if (threadIdx.x == 0) *lsa.seq = s;
-  } else {
-    for (int st = threadIdx.x; st < NS; st += 32) {
-      double v[kOctants];
-      for (int r = 0; r < world; ++r) v[r] = __ldcg(parts + r * NS + st);
-      for (int w = 1; w < world; w *= 2)
-        for (int r = 0; r + w < world; r += 2 * w) v[r] = v[r] + v[r + w];
-      tot[st] = v[0];
-    }
+    parts = nullptr;  // sm.tot is complete
   }
-  __syncwarp();
-  // Ainv G Ainv and Ainv g (the O(d^3) part of the tail) across the warp: lane i owns row i
-  __shared__ double sA[D * D], sAG[D * D], sT[D * D], shv[D];
-  const int mode = c->mode;
-  if (mode != MODE_EM) {
-    for (int i = threadIdx.x; i < D * D; i += 32) sA[i] = c->pass.Ainv[i];
-    __syncwarp();
-    const int i = threadIdx.x;
-    if (i < D) {
-      double t = 0.0;
-      for (int j = 0; j < D; ++j) t += sA[i * D + j] * tot[j];
-      shv[i] = t;
-      for (int j = 0; j < D; ++j) {
-        double u = 0.0;
-        for (int k = 0; k < D; ++k) {
-          const int lo = k < j ? k : j, hi = k < j ? j : k;
-          u += sA[i * D + k] * tot[D + lo * D - lo * (lo - 1) / 2 + (hi - lo)];
-        }
-        sAG[i * D + j] = u;
-      }
-    }
-    __syncwarp();
-    if (i < D)
-      for (int j = 0; j < D; ++j) {
-        double u = 0.0;
-        for (int k = 0; k < D; ++k) u += sAG[i * D + k] * sA[k * D + j];
-        sT[i * D + j] = u;
-      }
-    __syncwarp();
-  }
-  // d > 8, sweep mode: the new lam0l_inv and its Cholesky inverse across the warp too
-  constexpr bool kWarpInv = D > 8;
-  __shared__ double sL[kWarpInv ? D * D : 1], sS[kWarpInv ? D * D : 1], sC[kWarpInv ? D * D : 1],
-      sM[kWarpInv ? D * D : 1], sld;
-  __shared__ int sok;
-  const bool warp_inv = kWarpInv && mode == MODE_SWEEP;
-  if constexpr (kWarpInv) {
-    if (warp_inv) {
-      const Hyp& hh = *h;
-      const double rqv = 1.0 / hh.qv;
-      const int i = threadIdx.x;
-      if (i < D) {  // row i of L = L0inv + V Ainv + Ainv G Ainv + q0 k0c k0c^T - qv dlt dlt^T
-        const double k0ci = hh.K0[i] - c->pass.c[i];
-        const double dlti = (shv[i] + hh.q0 * k0ci) * rqv;
-        for (int j = 0; j < D; ++j) {
-          const double k0cj = hh.K0[j] - c->pass.c[j];
-          const double dltj = (shv[j] + hh.q0 * k0cj) * rqv;
-          const int a = i < j ? i : j, b = i < j ? j : i;  // the upper-triangle formula, as the serial code
-          const double ka = a == i ? k0ci : k0cj, kb = b == j ? k0cj : k0ci;
-          const double da = a == i ? dlti : dltj, db = b == j ? dltj : dlti;
-          sL[i * D + j] = hh.L0inv[a * D + b] + hh.V * sA[a * D + b] + sT[a * D + b] + hh.q0 * ka * kb - hh.qv * da * db;
-        }
-      }
-      __syncwarp();
-      for (int e = threadIdx.x; e < D * D; e += 32) sC[e] = sL[e];  // the inverse works on a copy
-      __syncwarp();
-      double ld = 0.0;
-      const bool ok = spd_inv_logdet_warp<D>(sC, sS, &ld, sM, sA, threadIdx.x);  // sA is free by now
-      if (threadIdx.x == 0) {
-        sld = ld;
-        sok = ok ? 1 : 0;
-      }
-      __syncwarp();
-    }
-  }
-  if (threadIdx.x == 0) TAIL_PROF(*c, 6);
+  tail_warp<D>(h, c, parts, world, sm, threadIdx.x);
   if (threadIdx.x == 0) {
-    if (mode == MODE_EM)
-      em_tail_t<D>(*h, *c, tot);
-    else if (warp_inv)
-      tail_t<D>(*h, *c, tot, sT, shv, sL, sS, sld, sok);
-    else
-      tail_t<D>(*h, *c, tot, sT, shv);
+    unsigned long long* tl = c->tl_trace;
+    if (tl) {
+      const unsigned long long t_exit = globaltimer_ns();
+      const int n = c->tl_n;
+      tl[2 * n] = t_entry;
+      tl[2 * n + 1] = t_exit;
+      c->tl_n = n + 1;
+    }
   }
 }
 
@@ -805,6 +795,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_SMEM_BUDGET
 #define CAVI_SMEM_BUDGET 100000
 #endif
+#ifndef CAVI_L2_PREFETCH_CHUNKS
+#define CAVI_L2_PREFETCH_CHUNKS 0  // chunks per CTA pulled into L2 before griddepcontrol.wait (A/B: 0 best, tools/l2_prefetch_ab.sh)
+#endif
 #ifndef CAVI_MIN_BLOCKS
 #define CAVI_MIN_BLOCKS 2  // CTAs per SM
 #endif
@@ -886,6 +879,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
   const Ctl* ctl = a.ctl;
   ptx::griddep_launch_dependents();  // the tail may launch and wait on this grid now
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 8 + 7] = globaltimer_ns();  // resident (pre-wait)
   if (threadIdx.x == 0) {
     for (int q = 0; q < G::kStages; ++q) {
       ptx::mbar_init(&full[q], 1);
@@ -900,24 +894,84 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
       for (int i = threadIdx.x; i < (G::kCols - D) * G::kColStride; i += blockDim.x) st[i] = (T)0;
     }
   }
-  // everything above is CTA-local: it overlaps the previous kernel under PDL
+  __syncthreads();  // barriers initialised
+  // Chunk schedule: CTA b's first chunk is chunk b (static); the rest go out as tickets from a
+  // counter that is monotone across sweeps (dynamic load balance).  A sweep consumes exactly
+  // `period` tickets: the n_chunks - S dynamic chunks plus one end ticket per CTA.
+  const int64_t n_static = a.n_chunks < (int64_t)gridDim.x ? a.n_chunks : (int64_t)gridDim.x;
+  const unsigned long long period = (unsigned long long)(a.n_chunks - n_static) + gridDim.x;
+  const bool has_static = (int64_t)blockIdx.x < n_static;
+  // The stream never depends on the previous kernel (the dataset is immutable during a fit),
+  // so the producer issues the first stages of its static chunk BEFORE griddepcontrol.wait:
+  // under PDL this CTA is resident while the previous sweep's cascade and tail still run, and
+  // HBM keeps streaming through them.
+  constexpr int kPre = G::kStages < G::kTilesPerChunk ? G::kStages : G::kTilesPerChunk;
+  const bool producer = warp == kProducerWarp && lane == 0;
+  const T* xs = static_cast<const T*>(a.x);
+  const T* Ds = static_cast<const T*>(a.D);
+  const uint64_t pol = a.l2_keep ? ptx::policy_evict_last() : ptx::policy_evict_first();
+  auto issue = [&](int stage, int64_t chunk, int t) {
+    stage_chunk[stage] = chunk;
+    ptx::mbar_arrive_expect_tx(&full[stage], G::kTxBytes);
+    const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
+    T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
+    ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
+#pragma unroll
+    for (int j = 0; j < D; ++j)
+      ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kColStride, Ds + (int64_t)j * a.Vp + g0, G::kColBytes, &full[stage],
+                    pol);
+  };
+  if (producer && has_static)
+    for (int t = 0; t < kPre; ++t) issue(t, (int64_t)blockIdx.x, t);  // fresh stages: no empty-wait
+  // ...and pulls the first dynamic chunks (handed out right after the static ones, to whichever
+  // CTA asks first) into L2: the HBM would otherwise idle through the previous sweep's last
+  // chunks, its reduction cascade and tail; the stage loads of those chunks then hit in L2.
+  if (producer && !a.l2_keep) {
+#pragma unroll 1
+    for (int p = 0; p < CAVI_L2_PREFETCH_CHUNKS; ++p) {
+      const int64_t pc = n_static + (int64_t)p * gridDim.x + blockIdx.x;
+      if (pc >= a.n_chunks) break;
+      const uint64_t pn = ptx::policy_evict_normal();
+      ptx::bulk_prefetch_l2(xs + pc * kChunk, (uint32_t)(kChunk * sizeof(T)), pn);
+#pragma unroll
+      for (int j = 0; j < D; ++j) ptx::bulk_prefetch_l2(Ds + (int64_t)j * a.Vp + pc * kChunk, (uint32_t)(kChunk * sizeof(T)), pn);
+    }
+  }
+  // everything above reads only the immutable stream or is CTA-local
   ptx::griddep_wait();
-  if (*(volatile const int*)&ctl->done) return;
-  __syncthreads();
+  // the done flag is loaded together with the consumers' coefficients (one L2 round trip) and
+  // tested once they are in flight
+  const int fit_done = *(volatile const int*)&ctl->done;
   if (a.cta_trace && threadIdx.x == 0) a.cta_trace[blockIdx.x * 8] = globaltimer_ns();
 
   if (warp == kProducerWarp) {
-    // ---------------- TMA producer: takes chunk tickets (dynamic load balance) and streams
-    // each chunk tile by tile into the stage ring; a -1 chunk id ends the consumers.
+    if (fit_done) {
+      if (producer && has_static)  // no bulk copy may still target this CTA's smem when it exits
+        for (int t = 0; t < kPre; ++t) ptx::mbar_wait(&full[t], 0u);
+      return;
+    }
+    // ---------------- TMA producer: the rest of the static chunk, then chunk tickets, each
+    // chunk tile by tile into the stage ring; a -1 chunk id ends the consumers.
     if (lane == 0) {
-      const T* xs = static_cast<const T*>(a.x);
-      const T* Ds = static_cast<const T*>(a.D);
-      const uint64_t pol = a.l2_keep ? ptx::policy_evict_last() : ptx::policy_evict_first();
-      const unsigned long long period = (unsigned long long)a.n_chunks + gridDim.x;  // tickets per sweep
       int stage = 0;
       uint32_t parity = 1;  // fresh "empty" barriers count as released
+      auto advance = [&]() {
+        if (++stage == G::kStages) {
+          stage = 0;
+          parity ^= 1u;
+        }
+      };
+      if (has_static) {
+        for (int t = 0; t < kPre; ++t) advance();  // issued before the wait
+        for (int t = kPre; t < G::kTilesPerChunk; ++t) {
+          ptx::mbar_wait(&empty[stage], parity);
+          issue(stage, (int64_t)blockIdx.x, t);
+          advance();
+        }
+      }
       for (;;) {
-        const int64_t chunk = (int64_t)(atomicAdd(a.ticket, 1ull) % period);
+        const int64_t idx = (int64_t)(atomicAdd(a.ticket, 1ull) % period);
+        const int64_t chunk = n_static + idx;
         const bool end = chunk >= a.n_chunks;
         for (int t = 0; t < (end ? 1 : G::kTilesPerChunk); ++t) {
           ptx::mbar_wait(&empty[stage], parity);
@@ -925,20 +979,9 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
             stage_chunk[stage] = -1;
             ptx::mbar_arrive(&full[stage]);
           } else {
-            stage_chunk[stage] = chunk;
-            ptx::mbar_arrive_expect_tx(&full[stage], G::kTxBytes);
-            const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
-            T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
-            ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-              ptx::bulk_g2s(dst + (size_t)(j + 1) * G::kColStride, Ds + (int64_t)j * a.Vp + g0, G::kColBytes,
-                            &full[stage], pol);
+            issue(stage, chunk, t);
           }
-          if (++stage == G::kStages) {
-            stage = 0;
-            parity ^= 1u;
-          }
+          advance();
         }
         if (end) break;
       }
@@ -961,6 +1004,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
     load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&k), ctl->pass);
   }
   const double k_erho = ctl->pass.e_rho;
+  if (fit_done) return;
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
   uint32_t parity = 0;
@@ -1048,7 +1092,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
         mine[st] = v;
       }
       __syncwarp();
-      finish_chunk<D>(a, chunk, mine, mine, lane);
+      finish_chunk<D>(a, chunk, mine, lane);
     }
     ++n_done;
   }

@@ -23,31 +23,50 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 TESTS = os.path.join(REF, "tests")
 
-SELECT = ["test_vb.py", "test_em.py", "test_analysis.py", "test_cli.py::TestFit", "test_cli.py::TestBench",
-          "test_cli.py::TestDensity",
-          "test_acceptance.py::test_c01_synthetic_recovery", "test_acceptance.py::test_c04_vb_convergence_profile",
-          "test_acceptance.py::test_c05_em_ascent", "test_acceptance.py::test_c08_elbo_cross_validation"]
-DESELECT = {}
+SELECT = ["test_vb.py", "test_em.py", "test_analysis.py", "test_cli.py", "test_acceptance.py"]
+# not run: not on this path (the reference's own Gibbs / Boolean-network code, unchanged by
+# install()) or CPU-only criteria
+DESELECT = {
+    "test_acceptance.py::test_c02_five_k_sweep": "~2 min of the reference's CPU Gibbs sampler per run; its VB "
+                                                 "half is C01's machinery on 5 more datasets",
+    "test_acceptance.py::test_c06_gibbs_desk_scale": "Gibbs sampler only (not on the CAVI path)",
+    "test_acceptance.py::test_c09_parallel_correctness_scaling": "asserts that the reference's CPU thread pool "
+        "speeds up and that serial CPU time grows with V; on the drop-in both timings are GPU-flat (its "
+        "correctness gate, serial/parallel agreement at 1e-8, passes: plan is accepted and results are "
+        "worker-independent)",
+    "test_acceptance.py::test_c10_boolean_network_semantics": "Boolean networks only (not on the CAVI path)",
+}
+# fails in the reference itself with exactly this message (reference pkg/test_output.txt:283):
+# the 1e-8 relative-change clause needs ~1.7k sweeps on this regime, not 300
+EXPECTED_FAIL = {"test_c04_vb_convergence_profile": "did not reach 1e-8 within 300 sweeps: last change 2.58e-06"}
 
 
-def run_suite(tmp_path, select):
+def run_suite(tmp_path):
     xml = tmp_path / "ref.xml"
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, TESTS, os.path.join(ROOT, "tests"), ROOT]))
-    args = [sys.executable, "-m", "pytest", "-p", "refsuite_plugin", "-q", "-x", "--no-header", "-p", "no:cacheprovider",
-            f"--junitxml={xml}", "--rootdir", TESTS, *[os.path.join(TESTS, s) for s in select]]
+    args = [sys.executable, "-m", "pytest", "-p", "refsuite_plugin", "-q", "--no-header", "-p", "no:cacheprovider",
+            f"--junitxml={xml}", "--rootdir", TESTS, *SELECT]
     for k in DESELECT:
-        args += ["--deselect", os.path.join(TESTS, k)]
+        args += ["--deselect", k]
     out = subprocess.run(args, cwd=TESTS, env=env, capture_output=True, text=True, timeout=1800)
     return out, ET.parse(xml).getroot() if xml.exists() else None
 
 
 @pytest.mark.skipif(not os.path.isdir(TESTS), reason="baseline/_ref not installed (tools/install_reference.sh)")
 def test_reference_suite_passes_on_the_drop_in(tmp_path):
-    out, root = run_suite(tmp_path, SELECT)
+    out, root = run_suite(tmp_path)
     assert root is not None, out.stdout[-3000:] + out.stderr[-3000:]
-    cases = root.iter("testcase")
-    failed = [f"{c.get('classname')}::{c.get('name')}" for c in cases
-              if c.find("failure") is not None or c.find("error") is not None]
-    n = int(sum(int(s.get("tests", 0)) for s in root.iter("testsuite")))
-    assert out.returncode == 0 and not failed, "\n".join(failed) + "\n" + out.stdout[-6000:]
-    assert n >= 60, f"only {n} reference tests ran"
+    failed, n = [], 0
+    for c in root.iter("testcase"):
+        n += 1
+        bad = c.find("failure") if c.find("failure") is not None else c.find("error")
+        if bad is None:
+            continue
+        want = EXPECTED_FAIL.get(c.get("name"))
+        text = (bad.get("message") or "") + (bad.text or "") + "".join(
+            (x.text or "") for x in c.iter("system-out"))
+        if want is not None and want in text:
+            continue  # the reference's own outcome, reproduced
+        failed.append(f"{c.get('classname')}::{c.get('name')}")
+    assert not failed, "\n".join(failed) + "\n" + out.stdout[-6000:]
+    assert n >= 80, f"only {n} reference tests ran"
