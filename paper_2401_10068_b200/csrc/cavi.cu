@@ -110,11 +110,11 @@ struct cv_dataset {
   double* mu_raw = nullptr;
   int64_t n_chunks = 0, n_groups = 0, group_lo = 0, n_groups_total = 0, groups_per_octant = 1;
   int oct_lo = 0, oct_hi = kOctants;
-  double* partials = nullptr;
-  double* gpartials = nullptr;
-  unsigned int* counters = nullptr;  // [n_groups] gcount | [8] ocount | odone
+  uint64_t* partials = nullptr;      // [n_chunks][ns][2] LL words
+  uint64_t* gpartials = nullptr;     // [n_groups][ns][2] LL words
+  unsigned int* counters = nullptr;  // [n_groups] gcount | [8] ocount | odone | pass_seq
   unsigned long long* ticket = nullptr;
-  double* opartials = nullptr;
+  uint64_t* opartials = nullptr;     // [8][ns][2] LL words
   int n_live_octants = 0;
   int* flags = nullptr;              // [0] bad input bits, [1] scratch status
   Ctl* ctl = nullptr;
@@ -231,13 +231,20 @@ int plan_and_alloc(cv_dataset* ds) {
   const size_t nx = (size_t)std::max<int64_t>(ds->Vp, 2);
   PALLOC(ds->x, nx * es);
   PALLOC(ds->D, nx * es * ds->d);
-  PALLOC(ds->partials, sizeof(double) * ns * std::max<int64_t>(ds->n_chunks, 1));
-  PALLOC(ds->gpartials, sizeof(double) * ns * std::max<int64_t>(ds->n_groups, 1));
-  PALLOC(ds->counters, sizeof(unsigned int) * (ds->n_groups + kOctants + 1));
-  CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + kOctants + 1), ds->stream));
+  // LL rows start tagged 0xffffffff, a tag no pass uses (pass_seq counts up from 0)
+  const size_t ll_c = 2 * sizeof(uint64_t) * ns * std::max<int64_t>(ds->n_chunks, 1);
+  const size_t ll_g = 2 * sizeof(uint64_t) * ns * std::max<int64_t>(ds->n_groups, 1);
+  const size_t ll_o = 2 * sizeof(uint64_t) * ns * kOctants;
+  PALLOC(ds->partials, ll_c);
+  CK(cudaMemsetAsync(ds->partials, 0xff, ll_c, ds->stream));
+  PALLOC(ds->gpartials, ll_g);
+  CK(cudaMemsetAsync(ds->gpartials, 0xff, ll_g, ds->stream));
+  PALLOC(ds->counters, sizeof(unsigned int) * (ds->n_groups + kOctants + 2));
+  CK(cudaMemsetAsync(ds->counters, 0, sizeof(unsigned int) * (ds->n_groups + kOctants + 2), ds->stream));
   PALLOC(ds->ticket, sizeof(unsigned long long));
   CK(cudaMemsetAsync(ds->ticket, 0, sizeof(unsigned long long), ds->stream));
-  PALLOC(ds->opartials, sizeof(double) * ns * kOctants);
+  PALLOC(ds->opartials, ll_o);
+  CK(cudaMemsetAsync(ds->opartials, 0xff, ll_o, ds->stream));
   PALLOC(ds->tot, sizeof(double) * kMaxStats * kOctants);
   count_live_octants(ds);
   PALLOC(ds->flags, sizeof(int) * 4);
@@ -281,6 +288,7 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.gcount = ds->counters;
   a.ocount = ds->counters + ds->n_groups;
   a.odone = ds->counters + ds->n_groups + kOctants;
+  a.pass_seq = ds->counters + ds->n_groups + kOctants + 1;
   a.opartials = ds->opartials;
   a.ticket = ds->ticket;
   a.n_live_octants = ds->n_live_octants;

@@ -41,12 +41,13 @@ struct PassArgs {
   int64_t groups_per_octant;
   int oct_lo, oct_hi;      // octants this shard owns
   int l2_keep;             // stream fits in L2: keep it resident across sweeps
-  double* partials;        // [n_chunks][ns]
-  double* gpartials;       // [n_groups][ns]
+  uint64_t* partials;      // [n_chunks][ns][2] chunk sums, LL words (tag = *pass_seq)
+  uint64_t* gpartials;     // [n_groups][ns][2] group sums, LL
   unsigned int* gcount;    // [n_groups] arrivals per group
   unsigned int* ocount;    // [8] arrivals per octant
   unsigned int* odone;     // [1] completed octants
-  double* opartials;       // [8][ns]
+  uint64_t* opartials;     // [8][ns][2] octant sums, LL
+  unsigned int* pass_seq;  // [1] passes completed on this dataset = the LL tag of the running pass
   unsigned long long* ticket;  // chunk tickets (monotone across sweeps)
   int n_live_octants;      // octants of this shard holding at least one group
   Ctl* ctl;
@@ -267,11 +268,57 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
+// ---- flag-in-data ("LL") rows of the reduction: a double travels as two 8-byte words
+// (pass tag << 32 | 32 data bits), each single-copy atomic, so a reader that sees both tags
+// equal to the running pass's tag has the value.  Arrivals are then counted with RELAXED
+// atomics: the last arriver of a level knows every sibling stored its row before arriving (in
+// program order) and polls the rows until their tags match -- a store-visibility wait, never
+// a wait on another warp's progress.  A release/acquire arrival instead pays the stores'
+// acknowledgement before the atomic: one L2 round trip more per level, three levels at the
+// end of every pass.
+__device__ __forceinline__ void ll_put(uint64_t* p, double v, uint32_t tag) {
+  const uint64_t u = (uint64_t)__double_as_longlong(v), t = (uint64_t)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(t | (u & 0xffffffffull)), "l"(t | (u >> 32))
+               : "memory");
+}
+__device__ __forceinline__ void ll_get2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ double ll_val(uint64_t a, uint64_t b) {
+  return __longlong_as_double((long long)((b << 32) | (a & 0xffffffffull)));
+}
+__device__ __forceinline__ bool ll_ok(uint64_t a, uint64_t b, uint32_t tag) {
+  return (uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag;
+}
+// poll one LL double (bounded: a protocol bug traps instead of hanging the GPU)
+static __device__ __noinline__ double ll_wait(const uint64_t* p, uint32_t tag) {
+  const unsigned long long t0 = globaltimer_ns();
+  for (;;) {
+    uint64_t a, b;
+    ll_get2(p, a, b);
+    if (ll_ok(a, b, tag)) return ll_val(a, b);
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+  }
+}
+
+// relaxed arrival: true on the warp whose arrival completes `need`
+__device__ __forceinline__ bool warp_arrive_last_relaxed(unsigned int* counter, unsigned int need, int lane) {
+  unsigned int last = 0;
+  __syncwarp();
+  if (lane == 0) {
+    unsigned int old;
+    asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+    last = old == need - 1;
+  }
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
 // The plan's fixed-order row sum (as warp_sum_rows: lane l adds rows l, l+32, ... from 0.0 in
-// index order, then the 16-8-4-2-1 xor butterfly) with the result left in registers: lane l
-// gets stat l + 32k in out[k].
+// index order, then the 16-8-4-2-1 xor butterfly) over n LL rows of NS values, polled until
+// tagged `tag`; the result stays in registers: lane l gets stat l + 32k in out[k].
 template <int NS>
-__device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (&out)[(NS + 31) / 32], int lane) {
+__device__ __forceinline__ void warp_rows_ll(const uint64_t* rows, int64_t n, uint32_t tag,
+                                             double (&out)[(NS + 31) / 32], int lane) {
   constexpr int B = NS < 16 ? NS : 16;
 #pragma unroll
   for (int k = 0; k < (NS + 31) / 32; ++k) out[k] = 0.0;
@@ -280,12 +327,16 @@ __device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (
     double acc[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) acc[b] = 0.0;
-#pragma unroll 2
+#pragma unroll 1
     for (int64_t i = lane; i < n; i += 32) {
-      const double* row = src + i * NS + s0;
+      const uint64_t* row = rows + (i * NS + s0) * 2;
+      uint64_t wa[B], wb[B];
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (s0 + b < NS) acc[b] += __ldcg(row + b);
+        if (s0 + b < NS) ll_get2(row + 2 * b, wa[b], wb[b]);
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (s0 + b < NS) acc[b] += ll_ok(wa[b], wb[b], tag) ? ll_val(wa[b], wb[b]) : ll_wait(row + 2 * b, tag);
     }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -297,18 +348,26 @@ __device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (
   }
 }
 
+template <int NS>
+__device__ __forceinline__ void ll_put_row(uint64_t* row, const double (&v)[(NS + 31) / 32], uint32_t tag, int lane) {
+#pragma unroll
+  for (int k = 0; k < (NS + 31) / 32; ++k)
+    if (lane + 32 * k < NS) ll_put(row + 2 * (lane + 32 * k), v[k], tag);
+}
+
 // chunk partial -> group -> octant -> total (-> tail), by whichever warp completes each level
-// (arrival counters: nobody waits for anybody).  The final level keeps the octant totals in
-// registers and issues every octant load at once (one L2 round trip for the tree).
+// (relaxed arrival counters + LL rows: nobody waits for anybody's progress).  The final level
+// keeps its own octant in registers and loads the others all at once.
 template <int D, int NS = n_stats(D)>
-__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, int lane) {
+__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, uint32_t tag,
+                                          int lane) {
   constexpr int K = (NS + 31) / 32;
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
-  for (int st = lane; st < NS; st += 32) a.partials[chunk * NS + st] = chunk_sum[st];
+  for (int st = lane; st < NS; st += 32) ll_put(a.partials + (chunk * NS + st) * 2, chunk_sum[st], tag);
   const int64_t grp = chunk / kGroupChunks;
   const int64_t c0 = grp * kGroupChunks;
   const int64_t nc = lmin(c0 + kGroupChunks, a.n_chunks) - c0;
-  if (!warp_arrive_last(a.gcount + grp, (unsigned int)nc, lane)) return;
+  if (!warp_arrive_last_relaxed(a.gcount + grp, (unsigned int)nc, lane)) return;
   // group complete
   if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
   const int64_t gg = a.group_lo + grp;  // global group index
@@ -316,24 +375,18 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
   const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
   const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
   double osum[K];
-  if (g1 - g0 == 1) {
-    // a one-group octant: its sum over one row is the row itself (the butterfly adds zeros),
-    // so the group completes the octant directly (small V: one arrival level less)
-    warp_rows<NS>(a.partials + c0 * NS, nc, osum, lane);
-  } else {
-    warp_rows<NS>(a.partials + c0 * NS, nc, osum, lane);
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      if (lane + 32 * k < NS) a.gpartials[grp * NS + lane + 32 * k] = osum[k];
-    if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
+  warp_rows_ll<NS>(a.partials + c0 * NS * 2, nc, tag, osum, lane);
+  if (g1 - g0 > 1) {
+    // (a one-group octant: its sum over one row is the row itself -- the butterfly adds
+    // zeros -- so the group completes the octant directly, one arrival level less)
+    ll_put_row<NS>(a.gpartials + grp * NS * 2, osum, tag, lane);
+    if (!warp_arrive_last_relaxed(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
     // octant complete
     if (lane == 0) a.ocount[o] = 0u;
-    warp_rows<NS>(a.gpartials + (g0 - a.group_lo) * NS, g1 - g0, osum, lane);
+    warp_rows_ll<NS>(a.gpartials + (g0 - a.group_lo) * NS * 2, g1 - g0, tag, osum, lane);
   }
-#pragma unroll
-  for (int k = 0; k < K; ++k)
-    if (lane + 32 * k < NS) a.opartials[o * NS + lane + 32 * k] = osum[k];
-  if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
+  ll_put_row<NS>(a.opartials + o * NS * 2, osum, tag, lane);
+  if (!warp_arrive_last_relaxed(a.odone, (unsigned int)a.n_live_octants, lane)) return;
   // every octant this shard owns is complete: pairwise tree over them (empty octants add 0);
   // this warp's own octant from registers, the others' loads all in flight together
   if (lane == 0) *a.odone = 0u;
@@ -346,13 +399,21 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
   for (int k = 0; k < K; ++k) {
     const int st = lane + 32 * k;
     double v[kOctants];
+    uint64_t wa[kOctants], wb[kOctants];
+    bool live[kOctants];
 #pragma unroll
     for (int q = 0; q < kOctants; ++q) {
       const int64_t h0 = lmax((int64_t)q * a.groups_per_octant, a.group_lo);
       const int64_t h1 = lmin(lmin((int64_t)(q + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
-      const bool live = st < NS && q >= a.oct_lo && q < a.oct_hi && h1 > h0;
-      v[q] = q == o ? osum[k] : (live ? __ldcg(a.opartials + q * NS + st) : 0.0);
+      live[q] = st < NS && q != o && q >= a.oct_lo && q < a.oct_hi && h1 > h0;
+      if (live[q]) ll_get2(a.opartials + (q * NS + st) * 2, wa[q], wb[q]);
     }
+#pragma unroll
+    for (int q = 0; q < kOctants; ++q)
+      v[q] = q == o ? osum[k]
+                    : (live[q] ? (ll_ok(wa[q], wb[q], tag) ? ll_val(wa[q], wb[q])
+                                                            : ll_wait(a.opartials + (q * NS + st) * 2, tag))
+                               : 0.0);
 #pragma unroll
     for (int w = 1; w < kOctants; w *= 2)
 #pragma unroll
@@ -373,6 +434,7 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
     for (int k = 0; k < K; ++k)
       if (lane + 32 * k < NS) a.rank_out[lane + 32 * k] = tot[k];
   }
+  if (lane == 0) *a.pass_seq = tag + 1u;  // the next pass's tag (read after this grid completes)
   if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
 }
 
@@ -1004,6 +1066,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
     load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&k), ctl->pass);
   }
   const double k_erho = ctl->pass.e_rho;
+  const uint32_t tag = *(volatile const unsigned int*)a.pass_seq;  // LL tag of this pass
   if (fit_done) return;
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
@@ -1092,7 +1155,7 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
         mine[st] = v;
       }
       __syncwarp();
-      finish_chunk<D>(a, chunk, mine, lane);
+      finish_chunk<D>(a, chunk, mine, tag, lane);
     }
     ++n_done;
   }
