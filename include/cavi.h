@@ -93,6 +93,7 @@ typedef struct cv_state {
 
 typedef struct cv_dataset cv_dataset;
 typedef struct cv_comm cv_comm;
+typedef struct cv_batch cv_batch;
 
 /* ---- library ---------------------------------------------------------- */
 int32_t cv_abi_version(void);
@@ -219,9 +220,18 @@ int32_t cv_summarize(const double* K, const double* rho, const double* Lam, int6
 
 /* ---- many independent fits (BASELINE config 4) --------------------------- */
 /* vb_fit on each of n_fits datasets (genes [offsets[f], offsets[f+1]) of r, mu, D),
- * all with hyperparameters hp, one warp per fit on `device`.  out: n_fits states;
- * traces (optional): [n_fits][4][max_iter] = elbo, delta_k0k, delta_rho, delta_lam per
- * sweep (NaN past each fit's n_iter = out[f].n_iter). */
+ * all with hyperparameters hp, on `device` (a group of 8 lanes per fit: genes split across
+ * the group, the tail on its first lane).  cv_batch_run leaves the results in HBM, owned by
+ * the returned handle, and writes each fit's sweep count to n_iter (optional, [n_fits]);
+ * cv_batch_states copies the states of fits [lo, hi), cv_batch_traces their traces
+ * ([hi-lo][4][max_iter] = elbo, delta_k0k, delta_rho, delta_lam per sweep, NaN past n_iter).
+ * cv_batched_fit = run + copy everything + destroy (out: n_fits states; traces optional). */
+int32_t cv_batch_run(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
+                     int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+                     double param_tol, int32_t device, int32_t* n_iter, cv_batch** out);
+int32_t cv_batch_states(cv_batch* b, int64_t lo, int64_t hi, cv_state* out);
+int32_t cv_batch_traces(cv_batch* b, int64_t lo, int64_t hi, double* out);
+void cv_batch_destroy(cv_batch* b);
 int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
                        int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
                        double param_tol, int32_t device, cv_state* out, double* traces);

@@ -106,6 +106,11 @@ _SIGS = {
     "cv_em_step": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, _D, _D, _D, _D, _D]),
     "cv_batched_fit": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32,
                                    C.c_double, C.c_int32, C.c_double, C.c_int32, _P(CvState), _D]),
+    "cv_batch_run": (C.c_int32, [_D, _D, _D, _P(C.c_int64), C.c_int64, C.c_int32, _P(CvHyper), C.c_int32, C.c_double,
+                                 C.c_int32, C.c_double, C.c_int32, _P(C.c_int32), _P(C.c_void_p)]),
+    "cv_batch_states": (C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _P(CvState)]),
+    "cv_batch_traces": (C.c_int32, [C.c_void_p, C.c_int64, C.c_int64, _D]),
+    "cv_batch_destroy": (None, [C.c_void_p]),
     "cv_posterior_sample": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
                                         C.c_int64, C.c_double, C.c_double, _D, _D, C.c_int64, C.c_int32, _D, _D, _D,
                                         _P(C.c_uint64)]),

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <fcntl.h>
@@ -1645,10 +1646,33 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
   return CV_OK;
 }
 
-int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
-                       int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
-                       double param_tol, int32_t device, cv_state* out, double* traces) {
-  if (!r || !mu || !D || !offsets || !hp || !out) return fail(CV_ERR_ARG, "null pointer");
+}  // extern "C"
+
+struct cv_batch {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int64_t n_fits = 0;
+  int max_iter = 0;
+  Ctl* ctls = nullptr;
+  double* tr = nullptr;
+  std::vector<void*> bufs;  // pool allocations (stream-ordered)
+  ~cv_batch() {
+    if (st) {
+      for (void* q : bufs) cudaFreeAsync(q, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
+};
+
+namespace {
+
+// Runs every fit of a batch on the device; the states, traces and control blocks stay in HBM
+// (owned by `b`) until fetched.
+int batch_run(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits, int32_t d,
+              const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo, double param_tol,
+              int32_t device, cv_batch* b, int32_t* n_iter) {
+  if (!r || !mu || !D || !offsets || !hp) return fail(CV_ERR_ARG, "null pointer");
   if (n_fits < 1) return fail(CV_ERR_ARG, "no fits");
   if (max_iter < 1) return fail(CV_ERR_ARG, "max_iter must be >= 1");
   if (d < 1 || d > kMaxD || hp->d != d) return fail(CV_ERR_ARG, "hyperparams dim %d != dataset dim %d", hp->d, d);
@@ -1661,22 +1685,33 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
     if (!std::isfinite(D[i])) return fail(CV_ERR_NONFINITE, "non-finite values in A");
   PassKernel pk = pass_for(d, CV_STORE_F64);
   CK(cudaSetDevice(device));
-  CallScratch sc;
-  CK(cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking));
-  cudaStream_t st = sc.st;
+  b->device = device;
+  b->n_fits = n_fits;
+  b->max_iter = max_iter;
+  CK(cudaStreamCreateWithFlags(&b->st, cudaStreamNonBlocking));
+  cudaStream_t st = b->st;
+  auto palloc = [&](auto** p, size_t bytes) -> cudaError_t {
+    void* q = nullptr;
+    const cudaError_t e = pool_alloc(&q, bytes ? bytes : 16, st, device);
+    if (e == cudaSuccess) b->bufs.push_back(q);
+    *p = reinterpret_cast<std::remove_pointer_t<decltype(p)>>(q);
+    return e;
+  };
   double *dr, *dmu, *dD, *dtr;
   int64_t* doff;
   Hyp *base, *hyps;
   Ctl* ctls;
   // stream-ordered pool allocations: repeated batches reuse the HBM (release threshold max)
-  CK(sc.palloc(&dr, sizeof(double) * G, device));
-  CK(sc.palloc(&dmu, sizeof(double) * G, device));
-  CK(sc.palloc(&dD, sizeof(double) * G * d, device));
-  CK(sc.palloc(&doff, sizeof(int64_t) * (n_fits + 1), device));
-  CK(sc.palloc(&base, sizeof(Hyp), device));
-  CK(sc.palloc(&hyps, sizeof(Hyp) * n_fits, device));
-  CK(sc.palloc(&ctls, sizeof(Ctl) * n_fits, device));
-  CK(sc.palloc(&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, device));
+  CK(palloc(&dr, sizeof(double) * G));
+  CK(palloc(&dmu, sizeof(double) * G));
+  CK(palloc(&dD, sizeof(double) * G * d));
+  CK(palloc(&doff, sizeof(int64_t) * (n_fits + 1)));
+  CK(palloc(&base, sizeof(Hyp)));
+  CK(palloc(&hyps, sizeof(Hyp) * n_fits));
+  CK(palloc(&ctls, sizeof(Ctl) * n_fits));
+  CK(palloc(&dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits));
+  b->ctls = ctls;
+  b->tr = dtr;
   CK(cudaMemcpyAsync(dr, r, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * G * d, cudaMemcpyHostToDevice, st));
@@ -1698,23 +1733,99 @@ int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const
                                           param_tol, dtr);
   CK(cudaGetLastError());
   BatchArgs a{dr, dmu, dD, doff, n_fits, hyps, ctls};
-  const unsigned nb = (unsigned)((n_fits + kBatchThreads - 1) / kBatchThreads);
+  const unsigned nb = (unsigned)((n_fits + kBatchFitsPerCta - 1) / kBatchFitsPerCta);
+  const bool prof = getenv("CAVI_BATCH_PROF") != nullptr;  // diagnostics: the fit kernel alone (events)
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st));
+  }
   pk.batched<<<nb, kBatchThreads, 0, st>>>(a);
   CK(cudaGetLastError());
-  // states are the first member of each control block: one strided copy
-  CK(cudaMemcpy2DAsync(out, sizeof(cv_state), ctls, sizeof(Ctl), sizeof(cv_state), n_fits, cudaMemcpyDeviceToHost,
-                       st));
-  if (traces)
-    CK(cudaMemcpyAsync(traces, dtr, sizeof(double) * 4 * (size_t)max_iter * n_fits, cudaMemcpyDeviceToHost, st));
+  if (prof) {
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    fprintf(stderr, "batched_fit_kernel: %lld fits in %.3f ms\n", (long long)n_fits, ms);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   std::vector<int> status(n_fits);
   CK(cudaMemcpy2DAsync(status.data(), sizeof(int), &ctls[0].status, sizeof(Ctl), sizeof(int), n_fits,
                        cudaMemcpyDeviceToHost, st));
+  if (n_iter)
+    CK(cudaMemcpy2DAsync(n_iter, sizeof(int32_t), &ctls[0].cur.n_iter, sizeof(Ctl), sizeof(int32_t), n_fits,
+                         cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int64_t f = 0; f < n_fits; ++f) {
     if (status[f] == CV_ERR_IMPROPER) return fail(CV_ERR_IMPROPER, "fit %lld: Q(Lambda) is improper; dataset too small", (long long)f);
     if (status[f] != CV_OK) return fail(status[f], "fit %lld failed with status %d", (long long)f, status[f]);
   }
   return CV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cv_batch_run(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
+                     int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+                     double param_tol, int32_t device, int32_t* n_iter, cv_batch** out) {
+  if (!out) return fail(CV_ERR_ARG, "null pointer");
+  cv_batch* b = new cv_batch();
+  const int rc = batch_run(r, mu, D, offsets, n_fits, d, hp, max_iter, rel_tol, compute_elbo, param_tol, device, b,
+                           n_iter);
+  if (rc != CV_OK) {
+    std::string keep = g_err;
+    delete b;
+    g_err = keep;
+    return rc;
+  }
+  *out = b;
+  return CV_OK;
+}
+
+int32_t cv_batch_states(cv_batch* b, int64_t lo, int64_t hi, cv_state* out) {
+  if (!b || !out || lo < 0 || hi > b->n_fits || lo > hi) return fail(CV_ERR_ARG, "bad fit range");
+  if (hi == lo) return CV_OK;
+  CK(cudaSetDevice(b->device));
+  // states are the first member of each control block: one strided copy
+  CK(cudaMemcpy2DAsync(out, sizeof(cv_state), b->ctls + lo, sizeof(Ctl), sizeof(cv_state), hi - lo,
+                       cudaMemcpyDeviceToHost, b->st));
+  CK(cudaStreamSynchronize(b->st));
+  return CV_OK;
+}
+
+int32_t cv_batch_traces(cv_batch* b, int64_t lo, int64_t hi, double* out) {
+  if (!b || !out || lo < 0 || hi > b->n_fits || lo > hi) return fail(CV_ERR_ARG, "bad fit range");
+  if (hi == lo) return CV_OK;
+  CK(cudaSetDevice(b->device));
+  const size_t per = sizeof(double) * 4 * (size_t)b->max_iter;
+  CK(cudaMemcpyAsync(out, b->tr + (size_t)lo * 4 * b->max_iter, per * (size_t)(hi - lo), cudaMemcpyDeviceToHost,
+                     b->st));
+  CK(cudaStreamSynchronize(b->st));
+  return CV_OK;
+}
+
+void cv_batch_destroy(cv_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  delete b;
+}
+
+int32_t cv_batched_fit(const double* r, const double* mu, const double* D, const int64_t* offsets, int64_t n_fits,
+                       int32_t d, const cv_hyper* hp, int32_t max_iter, double rel_tol, int32_t compute_elbo,
+                       double param_tol, int32_t device, cv_state* out, double* traces) {
+  if (!out) return fail(CV_ERR_ARG, "null pointer");
+  cv_batch* b = nullptr;
+  int rc = cv_batch_run(r, mu, D, offsets, n_fits, d, hp, max_iter, rel_tol, compute_elbo, param_tol, device, nullptr,
+                        &b);
+  if (rc == CV_OK) rc = cv_batch_states(b, 0, n_fits, out);
+  if (rc == CV_OK && traces) rc = cv_batch_traces(b, 0, n_fits, traces);
+  cv_batch_destroy(b);
+  return rc;
 }
 
 int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, int32_t d, int32_t n0, double q0,

@@ -32,8 +32,8 @@ import numpy as np
 
 from . import _lib, linalg, model
 
-__all__ = ["VbState", "VbTrace", "install", "vb_elbo", "vb_fit", "vb_fit_many", "vb_init", "vb_posterior_sample",
-           "vb_step"]
+__all__ = ["VbState", "VbTrace", "install", "vb_elbo", "vb_fit", "vb_fit_concat", "vb_fit_many", "vb_init",
+           "vb_posterior_sample", "vb_step"]
 
 # ---------------------------------------------------------------- dataset residency
 _resident: dict[int, tuple] = {}
@@ -266,72 +266,108 @@ def vb_fit_many(datasets, hp, max_iter: int = 300, rel_tol: float = 1e-8, comput
                 param_tol: float = 1e-10, device: int | None = None):
     """vb_fit on many independent datasets at once (BASELINE config 4: tissue samples).
 
-    One thread per fit runs the whole CAVI loop in-kernel (csrc/batched.cuh).  Returns a
-    sequence of (VbState, VbTrace), each equal to what vb_fit(ds, hp, ...) returns for
+    A group of lanes per fit runs the whole CAVI loop in-kernel (csrc/batched.cuh).  Returns
+    a sequence of (VbState, VbTrace), each equal to what vb_fit(ds, hp, ...) returns for
     that dataset (within 1e-9, same iteration count).  The datasets must share N.
     """
     datasets = list(datasets)
     if not datasets:
         raise ValueError("no datasets")
-    if max_iter < 1:
-        raise ValueError("max_iter must be >= 1")
     # one concatenation per field (no per-dataset conversions: 1e4-1e5 datasets per call)
     try:
-        D = np.ascontiguousarray(np.concatenate([ds.D for ds in datasets], axis=0), dtype=np.float64)
+        D = np.concatenate([ds.D for ds in datasets], axis=0)
     except ValueError:
         raise ValueError("all datasets must have the same number of networks") from None
+    r = np.concatenate([ds.r for ds in datasets])
+    mu = np.concatenate([ds.mu for ds in datasets])
+    n = len(datasets)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.fromiter((len(ds.r) for ds in datasets), dtype=np.int64, count=n), out=offsets[1:])
+    return vb_fit_concat(r, mu, D, offsets, hp, max_iter=max_iter, rel_tol=rel_tol, compute_elbo=compute_elbo,
+                         param_tol=param_tol, device=device, datasets=datasets)
+
+
+def vb_fit_concat(r, mu, D, offsets, hp, max_iter: int = 300, rel_tol: float = 1e-8, compute_elbo: bool = True,
+                  param_tol: float = 1e-10, device: int | None = None, datasets=None):
+    """vb_fit_many on pre-concatenated arrays: fit f is genes [offsets[f], offsets[f+1]) of
+    r, mu, D (no per-dataset Python work at all).  Results stay in HBM until accessed."""
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    D = np.ascontiguousarray(D, dtype=np.float64)
     if D.ndim != 2:
         raise ValueError("all datasets must have the same number of networks")
     d = D.shape[1]
     hd = int(np.atleast_1d(hp.K0).shape[0])
     if hd != d:
         raise ValueError(f"hyperparams dim {hd} != dataset dim {d}")
-    r = np.ascontiguousarray(np.concatenate([ds.r for ds in datasets]), dtype=np.float64)
-    mu = np.ascontiguousarray(np.concatenate([ds.mu for ds in datasets]), dtype=np.float64)
-    n = len(datasets)
-    offsets = np.zeros(n + 1, dtype=np.int64)
-    np.cumsum(np.fromiter((len(ds.r) for ds in datasets), dtype=np.int64, count=n), out=offsets[1:])
-    if offsets[-1] != D.shape[0] or r.shape[0] != D.shape[0]:
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = offsets.shape[0] - 1
+    if n < 1:
+        raise ValueError("no datasets")
+    if offsets[-1] != D.shape[0] or r.shape[0] != D.shape[0] or mu.shape[0] != D.shape[0]:
         raise ValueError("r, mu and D of a dataset must have the same number of genes")
-    # result buffers without a zero fill (1e4 states = 90 MB): the device writes every byte
-    sbuf = np.empty(n * C.sizeof(_lib.CvState), dtype=np.uint8)
-    states = (_lib.CvState * n).from_buffer(sbuf)
-    tr = np.empty((n, 4, max_iter))
+    n_iter = np.empty(n, dtype=np.int32)
     hs, keep = _lib.hyper_struct(hp)
-    _lib.check(_lib.lib().cv_batched_fit(
+    h = C.c_void_p()
+    _lib.check(_lib.lib().cv_batch_run(
         _lib.dptr(r), _lib.dptr(mu), _lib.dptr(D), offsets.ctypes.data_as(C.POINTER(C.c_int64)), n, d,
         C.byref(hs), int(max_iter), float(rel_tol), int(bool(compute_elbo)), float(param_tol),
-        _lib.default_device() if device is None else device, states, _lib.dptr(tr)))
-    raw = sbuf.reshape(n, C.sizeof(_lib.CvState))
-    off = _lib.CvState.n_iter.offset
-    n_iter = raw[:, off:off + 4].copy().view(np.int32)[:, 0]
-    return FitBatch(datasets, states, tr, n_iter, hp)
+        _lib.default_device() if device is None else device, n_iter.ctypes.data_as(C.POINTER(C.c_int32)),
+        C.byref(h)))
+    return FitBatch(h.value, n_iter, int(max_iter), hp, datasets, (r, mu, D, offsets))
 
 
 class FitBatch(Sequence):
-    """The (VbState, VbTrace) pairs of a vb_fit_many call, built on access.
+    """The (VbState, VbTrace) pairs of a vb_fit_many call.  The states and traces stay in HBM
+    (cv_batch handle) and are copied out on access: one fit, a slice, or everything with
+    `states()` / `traces()` -- 1e4-1e5 fits per call would otherwise mean ~200 MB of host
+    buffers filled on every call whether or not they are read."""
 
-    Each state is a view of its slot in the batch's state buffer and each trace a view
-    of its rows in the trace buffer (no per-fit copies: 1e4-1e5 fits per call).
-    """
-
-    def __init__(self, datasets, states, tr, n_iter, hp):
-        self._ds, self._states, self._tr, self._n_iter, self._hp = datasets, states, tr, n_iter, hp
+    def __init__(self, handle, n_iter, max_iter, hp, datasets, arrays):
+        self._h = C.c_void_p(handle)
+        self._fin = weakref.finalize(self, _lib.lib().cv_batch_destroy, self._h)
+        self._n_iter, self._max_iter, self._hp = n_iter, max_iter, hp
+        self._ds, self._arrays = datasets, arrays
 
     def __len__(self) -> int:
-        return len(self._ds)
+        return int(self._n_iter.shape[0])
+
+    def _source(self, i):
+        if self._ds is not None:
+            return self._ds[i]
+        r, mu, D, off = self._arrays
+        lo, hi = int(off[i]), int(off[i + 1])
+        return model.Dataset(r=r[lo:hi], mu=mu[lo:hi], D=D[lo:hi], n_networks=D.shape[1] + 1)
+
+    def states(self, lo: int = 0, hi: int | None = None):
+        """CvState structs of fits [lo, hi) in one copy."""
+        hi = len(self) if hi is None else hi
+        out = (_lib.CvState * (hi - lo))()
+        _lib.check(_lib.lib().cv_batch_states(self._h, lo, hi, out))
+        return out
+
+    def traces(self, lo: int = 0, hi: int | None = None) -> np.ndarray:
+        """[hi-lo, 4, max_iter] = elbo, delta_k0k, delta_rho, delta_lam (NaN past n_iter)."""
+        hi = len(self) if hi is None else hi
+        tr = np.empty((hi - lo, 4, self._max_iter))
+        _lib.check(_lib.lib().cv_batch_traces(self._h, lo, hi, _lib.dptr(tr)))
+        return tr
 
     def __getitem__(self, i):
         if isinstance(i, slice):
-            return [self[j] for j in range(*i.indices(len(self)))]
+            lo, hi, step = i.indices(len(self))
+            return [self[j] for j in range(lo, hi, step)]
         if i < 0:
             i += len(self)
         if not 0 <= i < len(self):
             raise IndexError(i)
-        st = VbState(self._states[i], None, self._hp)
-        st._lazy["source"] = self._ds[i]
+        cs = self.states(i, i + 1)[0]
+        st = VbState(cs, None, self._hp)
+        st._lazy["source"] = self._source(i)
         k = int(self._n_iter[i])
-        t = self._tr[i]
+        t = self.traces(i, i + 1)[0]
         return st, VbTrace(elbo=t[0, :k], delta_k0k=t[1, :k], delta_rho=t[2, :k], delta_lam=t[3, :k])
 
     @property
