@@ -46,7 +46,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--genes", type=float, default=1e8)
     p.add_argument("--networks", type=int, default=4)
-    p.add_argument("--storage", choices=["f64", "f32"], default="f64")
+    p.add_argument("--storage", choices=["f64", "f32", "f32m"], default="f64",
+                   help="f32: fp32 stream, fp64 math; f32m: fp32 stream and fp32 per-gene math (d <= 7)")
     p.add_argument("--e2e-sweeps", type=int, default=0, help="0: the reference's vb_fit defaults")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
@@ -312,7 +313,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64" if args.storage == "f64" else "f64 (fp32 storage)", "data": "synthetic",
+        "dtype": {"f64": "f64", "f32": "f64 (fp32 storage)", "f32m": "f32 per gene, f64 sums (fp32 storage)"}[args.storage],
+        "data": "synthetic",
         "config": bench_config(V, N, args.storage),
         "step": "one fused E-pass over the HBM-resident stream + the on-device K/Lambda/rho tail with the bound",
         "generate_s": round(gen_s, 3),

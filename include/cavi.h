@@ -53,7 +53,8 @@ enum {
 /* storage layouts of the measurement stream in HBM */
 enum {
   CV_STORE_F64 = 0, /* x = r - mu and D as fp64 (exact) */
-  CV_STORE_F32 = 1  /* x and D stored as fp32, fp64 math (the optional fp32 path) */
+  CV_STORE_F32 = 1, /* x and D stored as fp32, fp64 math (the optional fp32 path) */
+  CV_STORE_F32M = 2 /* fp32 storage and fp32 per-gene math, fp64 sums (d <= 7; fp64 math above) */
 };
 
 /* Prior constants (reference model.py:126-151).  Host pointers, borrowed. */

@@ -17,7 +17,7 @@ MAX_D = 15
 MAX_D2 = MAX_D * MAX_D
 
 OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT, ERR_PEER = range(8)
-STORE_F64, STORE_F32 = 0, 1
+STORE_F64, STORE_F32, STORE_F32M = 0, 1, 2
 
 _LIB_PATH = os.environ.get("CAVI_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcavi.so"))
 

@@ -137,7 +137,8 @@ struct cv_dataset {
 
 namespace {
 
-size_t elem(int storage) { return storage == CV_STORE_F32 ? sizeof(float) : sizeof(double); }
+bool f32_stream(int storage) { return storage == CV_STORE_F32 || storage == CV_STORE_F32M; }
+size_t elem(int storage) { return f32_stream(storage) ? sizeof(float) : sizeof(double); }
 
 // Stream-ordered pool allocations for everything whose lifetime is a dataset: repeated
 // uploads (the end-to-end path) then reuse HBM instead of paying cudaMalloc/cudaFree of
@@ -764,7 +765,8 @@ static int new_dataset(int64_t V, int32_t d, int64_t gene_lo, int64_t V_total, i
   if (V < 0 || V_total < 1 || (V == 0 && V_total == 0)) return fail(CV_ERR_ARG, "empty dataset");
   if (V == 0 && gene_lo == 0 && V_total == 0) return fail(CV_ERR_ARG, "empty dataset");
   if (d < 1 || d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
-  if (storage != CV_STORE_F64 && storage != CV_STORE_F32) return fail(CV_ERR_ARG, "bad storage %d", storage);
+  if (storage != CV_STORE_F64 && storage != CV_STORE_F32 && storage != CV_STORE_F32M)
+    return fail(CV_ERR_ARG, "bad storage %d", storage);
   if (gene_lo < 0 || V_total < gene_lo + V) return fail(CV_ERR_ARG, "shard [%lld, %lld) outside %lld genes",
                                                       (long long)gene_lo, (long long)(gene_lo + V), (long long)V_total);
   cv_dataset* ds = new cv_dataset();
@@ -791,7 +793,7 @@ int32_t cv_dataset_create(const double* r, const double* mu, const double* D, in
   cv_dataset* ds = nullptr;
   int rc = new_dataset(V, d, gene_lo, V_total, storage, device, &ds);
   if (rc) return rc;
-  rc = storage == CV_STORE_F32 ? create_storage_kernels<float>(ds, r, mu, D)
+  rc = f32_stream(storage) ? create_storage_kernels<float>(ds, r, mu, D)
                                : create_storage_kernels<double>(ds, r, mu, D);
   if (rc) {
     std::string keep = g_err;
@@ -859,7 +861,7 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
   }
   const int tb = 256;
   const unsigned blocks = (unsigned)((ds->Vp + tb - 1) / tb);
-  if (blocks > 0 && storage == CV_STORE_F32)
+  if (blocks > 0 && f32_stream(storage))
     gen_kernel<float><<<blocks, tb, 0, ds->stream>>>(a, dL);
   else if (blocks > 0)
     gen_kernel<double><<<blocks, tb, 0, ds->stream>>>(a, dL);
@@ -880,7 +882,7 @@ int32_t cv_dataset_download(cv_dataset* ds, double* x, double* r, double* mu, do
   const int tb = 256;
   const unsigned blocks = (unsigned)((ds->V + tb - 1) / tb);
   if (x || D) {
-    if (ds->storage == CV_STORE_F32)
+    if (f32_stream(ds->storage))
       download_kernel<float><<<blocks, tb, 0, ds->stream>>>((const float*)ds->x, (const float*)ds->D, ds->V, ds->Vp,
                                                             ds->d, dx, dD);
     else
@@ -1378,7 +1380,7 @@ int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, c
   const unsigned long long init[2] = {~0ull, 0ull};
   if (cudaMemcpy(dkeys, init, sizeof init, cudaMemcpyHostToDevice) != cudaSuccess)
     return bail(fail(CV_ERR_CUDA, "cudaMemcpy"));
-  rc = storage == CV_STORE_F32 ? parse_into<float>(ds, dtext, dterm, drow, L, N, dkeys, dslow, slow_cap)
+  rc = f32_stream(storage) ? parse_into<float>(ds, dtext, dterm, drow, L, N, dkeys, dslow, slow_cap)
                                : parse_into<double>(ds, dtext, dterm, drow, L, N, dkeys, dslow, slow_cap);
   if (rc) return bail(rc);
   unsigned long long keys[2];
@@ -1405,7 +1407,7 @@ int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, c
       int64_t row = 0;
       if (cudaMemcpy(&row, drow + l, sizeof row, cudaMemcpyDeviceToHost) != cudaSuccess)
         return bail(fail(CV_ERR_CUDA, "cudaMemcpy"));
-      rc = storage == CV_STORE_F32 ? put_row<float>(ds, row, v, N) : put_row<double>(ds, row, v, N);
+      rc = f32_stream(storage) ? put_row<float>(ds, row, v, N) : put_row<double>(ds, row, v, N);
       if (rc) return bail(rc);
     }
   }
@@ -1632,7 +1634,7 @@ int32_t cv_materialize(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, i
     if (hosts[q]) CK(sc.alloc(&outs[q], sizeof(double) * n * per[q]));
   const int tb = 128;
   const unsigned blocks = (unsigned)((n + tb - 1) / tb);
-  if (ds->storage == CV_STORE_F32)
+  if (f32_stream(ds->storage))
     materialize_kernel<float><<<blocks, tb, 0, ds->stream>>>((const float*)ds->x, (const float*)ds->D, ds->Vp, d, lo, n,
                                                              ds->ctl, outs[0], outs[1], outs[2], outs[3], outs[4]);
   else

@@ -122,6 +122,68 @@ __device__ __forceinline__ void load_coef(GeneCoef<D>& k, const Gen& g) {
   k.erho = g.e_rho;
 }
 
+// The optional fp32-math stream (CV_STORE_F32M): fp32 storage AND fp32 per-gene arithmetic,
+// the per-thread tile sums (8 genes) promoted to the fp64 accumulators, the den product in
+// fp64 -- SURVEY 7.7's fp32 variant, parity 1e-4 (the fp64 statistics are sums of ~1e-7
+// relative per-gene terms).  Same algebra as gene<D>(); resid uses e = (x - t)/den
+// (= x - t - s w exactly, no cancellation in fp32).
+template <int D>
+struct GeneCoefF {
+  float c[D];
+  float A2[D * (D + 1) / 2];
+  float erho;
+};
+
+template <int D>
+__device__ __forceinline__ void load_coef_f(GeneCoefF<D>& k, const Gen& g) {
+#pragma unroll
+  for (int j = 0; j < D; ++j) k.c[j] = (float)g.c[j];
+  int p = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int q = j; q < D; ++q) k.A2[p++] = (float)((q == j ? 1.0 : 2.0) * g.Ainv[j * D + q]);
+  k.erho = (float)g.e_rho;
+}
+
+template <int D>
+__device__ __forceinline__ float gene_f(const GeneCoefF<D>& k, float x, const float (&Dv)[D],
+                                        float (&acc)[n_stats(D)]) {
+  float t = 0.f, s = 0.f;
+#pragma unroll
+  for (int j = 0; j < D; ++j) t = fmaf(k.c[j], Dv[j], t);
+  {
+    int p = 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      float r = 0.f;
+#pragma unroll
+      for (int q = j; q < D; ++q) r = fmaf(k.A2[p++], Dv[q], r);
+      s = fmaf(Dv[j], r, s);
+    }
+  }
+  const float den = fmaf(k.erho, s, 1.f);
+  float inv;  // MUFU reciprocal (~1 ulp): the fp32 stream's budget is 1e-4
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(den));
+  const float xt = x - t;
+  const float ei = k.erho * inv;
+  const float w = ei * xt;
+  const float gam = fmaf(w, w, -ei);
+  const float e = xt * inv;
+  acc[stat_R(D)] += fmaf(e, e, s * inv);
+  acc[stat_Q(D)] = fmaf(w, xt, acc[stat_Q(D)]);
+#pragma unroll
+  for (int j = 0; j < D; ++j) acc[j] = fmaf(w, Dv[j], acc[j]);
+  int p = 0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const float gd = gam * Dv[j];
+#pragma unroll
+    for (int q = j; q < D; ++q, ++p) acc[D + p] = fmaf(gd, Dv[q], acc[D + p]);
+  }
+  return den;
+}
+
 // one gene: accumulate its statistics, return den
 template <int D>
 __device__ __forceinline__ double gene(const GeneCoef<D>& k, double x, const double (&Dv)[D],
@@ -857,6 +919,15 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_SMEM_BUDGET
 #define CAVI_SMEM_BUDGET 100000
 #endif
+#ifndef CAVI_F32_BLOCKS
+#define CAVI_F32_BLOCKS 3  // CTAs per SM on the fp32 stream, fp64 math (V=1e8 N=4: 2 -> 3: 2178 -> 2475 sweeps/s)
+#endif
+#ifndef CAVI_F32M_BLOCKS
+#define CAVI_F32M_BLOCKS 3  // ... and with fp32 math (2 -> 4: 2272 -> 3034 sweeps/s; + 16-byte loads, MUFU rcp: 3546 at 4, 3542 at 3)
+#endif
+#ifndef CAVI_F32_BLOCKS_MAXD
+#define CAVI_F32_BLOCKS_MAXD 3
+#endif
 #ifndef CAVI_L2_PREFETCH_CHUNKS
 #define CAVI_L2_PREFETCH_CHUNKS 0  // chunks per CTA pulled into L2 before griddepcontrol.wait (A/B: 0 best, tools/l2_prefetch_ab.sh)
 #endif
@@ -878,7 +949,7 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #define CAVI_MMA_CONS 128  // consumer threads per CTA on the DMMA path
 #endif
 
-template <int D, typename T>
+template <int D, typename T, typename M = double>
 struct Geometry {
   static constexpr bool kMma = D >= CAVI_MMA_MIN_D;
   static constexpr int kCons = kMma ? CAVI_MMA_CONS : CAVI_CONS;
@@ -904,6 +975,8 @@ struct Geometry {
   static constexpr int kSlotBytes = kSlots * kCWarps * kNS * 8;
   // the DMMA kernels at d <= 8 (~110 registers) are latency-bound at 2 CTAs/SM: run 3
   static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS
+                                   : (sizeof(T) == 4 && sizeof(M) == 4 && D <= CAVI_F32_BLOCKS_MAXD) ? CAVI_F32M_BLOCKS
+                                   : (sizeof(T) == 4 && D <= CAVI_F32_BLOCKS_MAXD) ? CAVI_F32_BLOCKS
                                    : D <= 1     ? CAVI_TINY_BLOCKS
                                    : D == 2     ? CAVI_D2_BLOCKS
                                    : D == 4     ? CAVI_D4_BLOCKS
@@ -922,9 +995,12 @@ struct Geometry {
   static_assert(kStages <= (kSlots - 1) * kTilesPerChunk, "warp drift could lap the reduction slots");
 };
 
-template <int D, typename T>
-__global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::kMinBlocks) pass_kernel(PassArgs a) {
-  using G = Geometry<D, T>;
+template <int D, typename T, typename M = double>
+__global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T, M>::kMinBlocks)
+    pass_kernel(PassArgs a) {
+  using G = Geometry<D, T, M>;
+  // fp32 per-gene math on the register path (CV_STORE_F32M); the DMMA path stays fp64
+  constexpr bool kF32Math = sizeof(M) == 4 && !G::kMma;
   constexpr int NS = n_stats(D);
   constexpr int kWarps = G::kCWarps;
   constexpr int kThreads = G::kCons;
@@ -1055,16 +1131,18 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
   // ---------------- consumers: independent warps, no CTA barrier in the steady state
   constexpr bool kSmemCoef = !G::kMma && D >= CAVI_SMEM_COEF_MIN_D;
   __shared__ GeneCoef<kSmemCoef ? D : 1> s_coef[kSmemCoef ? kWarps : 1];
-  GeneCoef<(G::kMma || kSmemCoef ? 1 : D)> k;
+  GeneCoef<(G::kMma || kSmemCoef || kF32Math ? 1 : D)> k;
   MmaConsumer<D> mc;
   if constexpr (G::kMma) {
     mc.load(ctl->pass, lane);
   } else if constexpr (kSmemCoef) {
     if (lane == 0) load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&s_coef[warp]), ctl->pass);
     __syncwarp();
-  } else {
+  } else if constexpr (!kF32Math) {
     load_coef<D>(*reinterpret_cast<GeneCoef<D>*>(&k), ctl->pass);
   }
+  GeneCoefF<kF32Math ? D : 1> kf;
+  if constexpr (kF32Math) load_coef_f<D>(kf, ctl->pass);
   const double k_erho = ctl->pass.e_rho;
   const uint32_t tag = *(volatile const unsigned int*)a.pass_seq;  // LL tag of this pass
   if (fit_done) return;
@@ -1103,19 +1181,72 @@ __global__ void __launch_bounds__(Geometry<D, T>::kCtaThreads, Geometry<D, T>::k
         if (t) ptx::mbar_wait(&full[stage], parity);
         const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
         double prod = 1.0;
+        if constexpr (kF32Math) {  // fp32 per gene, the tile's sums promoted to the fp64 accumulators
+          // 16-byte shared loads: this thread's genes come in runs of 4 (a warp reads 512
+          // contiguous bytes per column: conflict-free), 4x fewer load instructions per gene
+          static_assert(G::kGenesPerThread % 4 == 0, "vector loads need runs of 4 genes");
+          float a32[NS];
 #pragma unroll
-        for (int u = 0; u < G::kGenesPerThread; ++u) {
-          const int gi = u * kThreads + tid;
-          double Dv[D];
+          for (int i = 0; i < NS; ++i) a32[i] = 0.f;
 #pragma unroll
-          for (int j = 0; j < D; ++j) Dv[j] = (double)tile[(j + 1) * G::kColStride + gi];
-          if constexpr (kSmemCoef)
-            prod *= gene_rows<D>(SmemCoef<D>{reinterpret_cast<const volatile GeneCoef<D>*>(&s_coef[warp]), k_erho},
-                                 (double)tile[gi], Dv, acc);
-          else if constexpr (D >= CAVI_ROWFORM_MIN_D)
-            prod *= gene_rows<D>(RegCoef<D>{*reinterpret_cast<const GeneCoef<D>*>(&k)}, (double)tile[gi], Dv, acc);
-          else
-            prod *= gene<D>(*reinterpret_cast<const GeneCoef<D>*>(&k), (double)tile[gi], Dv, acc);
+          for (int u4 = 0; u4 < G::kGenesPerThread / 4; ++u4) {
+            const int g4 = (u4 * kThreads + tid) * 4;
+            const float4 xv = *reinterpret_cast<const float4*>(tile + g4);
+            float4 dv[D];
+#pragma unroll
+            for (int j = 0; j < D; ++j) dv[j] = *reinterpret_cast<const float4*>(tile + (j + 1) * G::kColStride + g4);
+            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float Dv[D];
+#pragma unroll
+              for (int j = 0; j < D; ++j) Dv[j] = v == 0 ? dv[j].x : v == 1 ? dv[j].y : v == 2 ? dv[j].z : dv[j].w;
+              prod *= (double)gene_f<D>(kf, xs[v], Dv, a32);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < NS; ++i)
+            if (i != stat_Ld(D)) acc[i] += (double)a32[i];
+        } else {
+          auto one = [&](double x, const double (&Dv)[D]) {
+            if constexpr (kSmemCoef)
+              prod *= gene_rows<D>(SmemCoef<D>{reinterpret_cast<const volatile GeneCoef<D>*>(&s_coef[warp]), k_erho},
+                                   x, Dv, acc);
+            else if constexpr (D >= CAVI_ROWFORM_MIN_D)
+              prod *= gene_rows<D>(RegCoef<D>{*reinterpret_cast<const GeneCoef<D>*>(&k)}, x, Dv, acc);
+            else
+              prod *= gene<D>(*reinterpret_cast<const GeneCoef<D>*>(&k), x, Dv, acc);
+          };
+          if constexpr (sizeof(T) == 4 && G::kGenesPerThread % 4 == 0) {
+            // fp32 stream, fp64 math: 16-byte shared loads as on the fp32-math path
+#pragma unroll
+            for (int u4 = 0; u4 < G::kGenesPerThread / 4; ++u4) {
+              const int g4 = (u4 * kThreads + tid) * 4;
+              const float4 xv = *reinterpret_cast<const float4*>(tile + g4);
+              float4 dv[D];
+#pragma unroll
+              for (int j = 0; j < D; ++j)
+                dv[j] = *reinterpret_cast<const float4*>(tile + (j + 1) * G::kColStride + g4);
+              const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                double Dv[D];
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                  Dv[j] = (double)(v == 0 ? dv[j].x : v == 1 ? dv[j].y : v == 2 ? dv[j].z : dv[j].w);
+                one((double)xs[v], Dv);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < G::kGenesPerThread; ++u) {
+              const int gi = u * kThreads + tid;
+              double Dv[D];
+#pragma unroll
+              for (int j = 0; j < D; ++j) Dv[j] = (double)tile[(j + 1) * G::kColStride + gi];
+              one((double)tile[gi], Dv);
+            }
+          }
         }
         lg.mul(prod);
         __syncwarp();

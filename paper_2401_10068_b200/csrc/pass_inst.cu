@@ -11,11 +11,11 @@
 #define CAVI_CAT2(a, b) a##b
 #define CAVI_CAT(a, b) CAVI_CAT2(a, b)
 
-template <typename T>
+template <typename T, typename M = double>
 static cavi::PassKernel make_kernel() {
-  using G = cavi::Geometry<CAVI_D, T>;
+  using G = cavi::Geometry<CAVI_D, T, M>;
   cavi::PassKernel k;
-  k.fn = cavi::pass_kernel<CAVI_D, T>;
+  k.fn = cavi::pass_kernel<CAVI_D, T, M>;
   k.threads = G::kCtaThreads;
   k.smem = G::kSmem;
   k.tail = cavi::tail_kernel<CAVI_D>;
@@ -27,5 +27,6 @@ static cavi::PassKernel make_kernel() {
 }
 
 cavi::PassKernel CAVI_CAT(cavi_pass_d, CAVI_D)(int storage) {
+  if (storage == CV_STORE_F32M) return make_kernel<float, float>();
   return storage == CV_STORE_F32 ? make_kernel<float>() : make_kernel<double>();
 }

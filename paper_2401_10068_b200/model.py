@@ -142,7 +142,8 @@ class DeviceDataset:
     Holds genes [gene_lo, gene_lo + V) of a dataset of V_total genes; for a
     single-GPU dataset gene_lo = 0 and V == V_total.  Layout: x = r - mu and
     the D columns, structure-of-arrays, fp64 (`storage="f64"`) or fp32
-    (`storage="f32"`, the optional fp32 path; math stays fp64).
+    (`storage="f32"`, the optional fp32 path; math stays fp64; `storage="f32m"`: fp32 per-gene
+    math as well, fp64 sums).
     """
 
     def __init__(self, handle: int, n_networks: int):
@@ -152,7 +153,7 @@ class DeviceDataset:
         _lib.check(_lib.lib().cv_dataset_info(self._h, C.byref(V), C.byref(d), C.byref(lo), C.byref(Vt),
                                               C.byref(st), C.byref(nb)))
         self.V, self.dim, self.gene_lo, self.V_total = V.value, d.value, lo.value, Vt.value
-        self.storage = "f32" if st.value == _lib.STORE_F32 else "f64"
+        self.storage = {_lib.STORE_F32: "f32", _lib.STORE_F32M: "f32m"}.get(st.value, "f64")
         self.device_bytes = nb.value
         self._fin = weakref.finalize(self, _lib.lib().cv_dataset_destroy, self._h)
 
@@ -180,7 +181,7 @@ class DeviceDataset:
         return x
 
 
-_STORAGE = {"f64": _lib.STORE_F64, "f32": _lib.STORE_F32}
+_STORAGE = {"f64": _lib.STORE_F64, "f32": _lib.STORE_F32, "f32m": _lib.STORE_F32M}
 
 
 def upload(ds, storage: str = "f64", device: int | None = None, gene_lo: int = 0, V_total: int | None = None):

@@ -117,6 +117,9 @@ def test_config3_headline_v1e8_matches_fused_oracle(eng):
     d32 = model.regime(V, 2026, N, storage="f32")
     s32, t32 = vb.vb_fit(d32, hp, max_iter=iters)
     d32.close()
+    d32m = model.regime(V, 2026, N, storage="f32m")
+    s32m, t32m = vb.vb_fit(d32m, hp, max_iter=iters)
+    d32m.close()
     so, to, n = _fused_fit_streamed(r, mu, D, N, iters)
     assert len(tr) == n == len(t32) == iters
     np.testing.assert_allclose(tr.elbo, to["elbo"], rtol=RTOL, atol=0)
@@ -126,7 +129,9 @@ def test_config3_headline_v1e8_matches_fused_oracle(eng):
     for name in ("b_rho", "k0k", "lam0l_inv", "e_lam", "e_rho"):
         close(getattr(st, name), getattr(so, name), RTOL, name)
         close(getattr(s32, name), getattr(so, name), RTOL32, name + " (fp32)")
+        close(getattr(s32m, name), getattr(so, name), RTOL32, name + " (fp32 math)")
     np.testing.assert_allclose(t32.elbo, to["elbo"], rtol=RTOL32, atol=0)
+    np.testing.assert_allclose(t32m.elbo, to["elbo"], rtol=RTOL32, atol=0)
 
 
 def test_config3_v1e7_matches_reference_oracle(eng):
@@ -164,6 +169,21 @@ def test_k_sweep_fp32_storage_matches_reference_oracle(eng, N, V, iters):
     r, mu, D, _, _ = philox.make_regime(V, 60 + N, N)
     ds = model.Dataset(r=r, mu=mu, D=D, n_networks=N)
     st, tr = vb.vb_fit(vb.device_dataset(ds, storage="f32"), model.default_hyperparams(N), max_iter=iters)
+    so, to = ocavi.fit(r, mu, D, ocavi.default_hyper(N), max_iter=iters)
+    check_fit(st, tr, so, to, RTOL32, deltas=False)
+
+
+@pytest.mark.parametrize("N,V,iters", [(2, 30000, 12), (3, 20000, 10), (4, 1_000_000, 25), (5, 8000, 8),
+                                       (7, 5000, 8), (8, 4000, 6), (9, 3000, 5)])
+def test_fp32_math_stream_matches_reference_oracle(eng, N, V, iters):
+    """storage="f32m" (fp32 per-gene math on the register path d <= 7, fp64 above): 1e-4 against
+    the direct reference restatement at a fixed sweep count."""
+    vb, model = eng
+    r, mu, D, _, _ = philox.make_regime(V, 80 + N, N)
+    ds = model.Dataset(r=r, mu=mu, D=D, n_networks=N)
+    dd = vb.device_dataset(ds, storage="f32m")
+    assert dd.storage == "f32m"
+    st, tr = vb.vb_fit(dd, model.default_hyperparams(N), max_iter=iters)
     so, to = ocavi.fit(r, mu, D, ocavi.default_hyper(N), max_iter=iters)
     check_fit(st, tr, so, to, RTOL32, deltas=False)
 
