@@ -30,6 +30,13 @@
 
 namespace cavi {
 
+#ifndef CAVI_LL_BATCH
+#define CAVI_LL_BATCH 16  // statistics per polling pass of an LL row sum
+#endif
+#ifndef CAVI_LL_MAX_D
+#define CAVI_LL_MAX_D 4  // largest d on the LL cascade (memory-bound); above: acquire/release rows (N=6: 1303 vs 1352)
+#endif
+
 struct PassArgs {
   const void* x;
   const void* D;
@@ -330,6 +337,122 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
+// The plan's fixed-order row sum (as warp_sum_rows: lane l adds rows l, l+32, ... from 0.0 in
+// index order, then the 16-8-4-2-1 xor butterfly) with the result left in registers: lane l
+// gets stat l + 32k in out[k].
+template <int NS>
+__device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (&out)[(NS + 31) / 32], int lane) {
+  constexpr int B = NS < 16 ? NS : 16;
+#pragma unroll
+  for (int k = 0; k < (NS + 31) / 32; ++k) out[k] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < NS; s0 += B) {
+    double acc[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = 0.0;
+#pragma unroll 2
+    for (int64_t i = lane; i < n; i += 32) {
+      const double* row = src + i * NS + s0;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (s0 + b < NS) acc[b] += __ldcg(row + b);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      double v = acc[b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (s0 + b < NS && (s0 + b) % 32 == lane) out[(s0 + b) / 32] = v;
+    }
+  }
+}
+
+// The same cascade with plain partial rows and acquire/release arrivals (the round-1 protocol),
+// kept for the compute-bound instantiations (d > CAVI_LL_MAX_D): there the LL version's
+// strong loads/stores and row buffers cost more in the consumer loop than the per-chunk release
+// fence they save (same-box A/B, V=1e8: N=8 824 vs 639 sweeps/s; N=4 488 vs 511 us the other
+// way).  The rows live in the LL buffers, read as doubles.
+template <int D, int NS = n_stats(D)>
+__device__ __forceinline__ void finish_chunk_acqrel(const PassArgs& a, int64_t chunk, const double* chunk_sum,
+                                                    int lane) {
+  double* const partials = reinterpret_cast<double*>(a.partials);
+  double* const gpartials = reinterpret_cast<double*>(a.gpartials);
+  double* const opartials = reinterpret_cast<double*>(a.opartials);
+  constexpr int K = (NS + 31) / 32;
+  const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
+  for (int st = lane; st < NS; st += 32) partials[chunk * NS + st] = chunk_sum[st];
+  const int64_t grp = chunk / kGroupChunks;
+  const int64_t c0 = grp * kGroupChunks;
+  const int64_t nc = lmin(c0 + kGroupChunks, a.n_chunks) - c0;
+  if (!warp_arrive_last(a.gcount + grp, (unsigned int)nc, lane)) return;
+  // group complete
+  if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
+  const int64_t gg = a.group_lo + grp;  // global group index
+  const int o = (int)(gg / a.groups_per_octant);
+  const int64_t g0 = lmax((int64_t)o * a.groups_per_octant, a.group_lo);
+  const int64_t g1 = lmin(lmin((int64_t)(o + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
+  double osum[K];
+  if (g1 - g0 == 1) {
+    // a one-group octant: its sum over one row is the row itself (the butterfly adds zeros),
+    // so the group completes the octant directly (small V: one arrival level less)
+    warp_rows<NS>(partials + c0 * NS, nc, osum, lane);
+  } else {
+    warp_rows<NS>(partials + c0 * NS, nc, osum, lane);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) gpartials[grp * NS + lane + 32 * k] = osum[k];
+    if (!warp_arrive_last(a.ocount + o, (unsigned int)(g1 - g0), lane)) return;
+    // octant complete
+    if (lane == 0) a.ocount[o] = 0u;
+    warp_rows<NS>(gpartials + (g0 - a.group_lo) * NS, g1 - g0, osum, lane);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (lane + 32 * k < NS) opartials[o * NS + lane + 32 * k] = osum[k];
+  if (!warp_arrive_last(a.odone, (unsigned int)a.n_live_octants, lane)) return;
+  // every octant this shard owns is complete: pairwise tree over them (empty octants add 0);
+  // this warp's own octant from registers, the others' loads all in flight together
+  if (lane == 0) *a.odone = 0u;
+  if (a.cta_trace && lane == 0) {
+    a.cta_trace[blockIdx.x * 8 + 4] = t_entry;
+    a.cta_trace[blockIdx.x * 8 + 5] = globaltimer_ns();
+  }
+  double tot[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int st = lane + 32 * k;
+    double v[kOctants];
+#pragma unroll
+    for (int q = 0; q < kOctants; ++q) {
+      const int64_t h0 = lmax((int64_t)q * a.groups_per_octant, a.group_lo);
+      const int64_t h1 = lmin(lmin((int64_t)(q + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
+      const bool live = st < NS && q >= a.oct_lo && q < a.oct_hi && h1 > h0;
+      v[q] = q == o ? osum[k] : (live ? __ldcg(opartials + q * NS + st) : 0.0);
+    }
+#pragma unroll
+    for (int w = 1; w < kOctants; w *= 2)
+#pragma unroll
+      for (int q = 0; q + w < kOctants; q += 2 * w)
+        if (q >= a.oct_lo && q + w < a.oct_hi && ((q - a.oct_lo) % (2 * w)) == 0) v[q] = v[q] + v[q + w];
+    tot[k] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kOctants; ++q)
+      if (q == a.oct_lo) tot[k] = v[q];
+  }
+  if (a.lsa.win) {  // fused exchange: straight into every peer's window over NVLink
+    const uint64_t sq = *a.lsa.seq + 1;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) lsa_publish_stat(a.lsa, sq, lane + 32 * k, tot[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane + 32 * k < NS) a.rank_out[lane + 32 * k] = tot[k];
+  }
+  if (lane == 0) *a.pass_seq += 1u;  // keep the LL tag in step (unused on this path)
+  if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
+}
+
 // ---- flag-in-data ("LL") rows of the reduction: a double travels as two 8-byte words
 // (pass tag << 32 | 32 data bits), each single-copy atomic, so a reader that sees both tags
 // equal to the running pass's tag has the value.  Arrivals are then counted with RELAXED
@@ -352,15 +475,10 @@ __device__ __forceinline__ double ll_val(uint64_t a, uint64_t b) {
 __device__ __forceinline__ bool ll_ok(uint64_t a, uint64_t b, uint32_t tag) {
   return (uint32_t)(a >> 32) == tag && (uint32_t)(b >> 32) == tag;
 }
-// poll one LL double (bounded: a protocol bug traps instead of hanging the GPU)
-static __device__ __noinline__ double ll_wait(const uint64_t* p, uint32_t tag) {
-  const unsigned long long t0 = globaltimer_ns();
-  for (;;) {
-    uint64_t a, b;
-    ll_get2(p, a, b);
-    if (ll_ok(a, b, tag)) return ll_val(a, b);
-    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
-  }
+// polls are bounded (a protocol bug traps instead of hanging the GPU); no function calls in
+// the pass kernel (an ABI call makes the compiler spill the consumer loop's live registers)
+__device__ __forceinline__ void ll_check_deadline(unsigned long long t0) {
+  if (globaltimer_ns() - t0 > 4000000000ull) __trap();
 }
 
 // relaxed arrival: true on the warp whose arrival completes `need`
@@ -381,7 +499,9 @@ __device__ __forceinline__ bool warp_arrive_last_relaxed(unsigned int* counter, 
 template <int NS>
 __device__ __forceinline__ void warp_rows_ll(const uint64_t* rows, int64_t n, uint32_t tag,
                                              double (&out)[(NS + 31) / 32], int lane) {
-  constexpr int B = NS < 16 ? NS : 16;
+  // stats per pass: small enough that the row words fit beside the consumer loop's live
+  // registers (this is inlined into it: a larger batch spills the loop state)
+  constexpr int B = NS < CAVI_LL_BATCH ? NS : CAVI_LL_BATCH;
 #pragma unroll
   for (int k = 0; k < (NS + 31) / 32; ++k) out[k] = 0.0;
 #pragma unroll
@@ -393,12 +513,23 @@ __device__ __forceinline__ void warp_rows_ll(const uint64_t* rows, int64_t n, ui
     for (int64_t i = lane; i < n; i += 32) {
       const uint64_t* row = rows + (i * NS + s0) * 2;
       uint64_t wa[B], wb[B];
+      unsigned long long t0 = 0;
+#pragma unroll 1
+      for (int tries = 0;; ++tries) {  // normally one pass: the siblings stored before arriving
+        bool ok = true;
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+          if (s0 + b < NS) ll_get2(row + 2 * b, wa[b], wb[b]);
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+          if (s0 + b < NS) ok = ok && ll_ok(wa[b], wb[b], tag);
+        if (ok) break;
+        if (tries == 0) t0 = globaltimer_ns();
+        ll_check_deadline(t0);
+      }
 #pragma unroll
       for (int b = 0; b < B; ++b)
-        if (s0 + b < NS) ll_get2(row + 2 * b, wa[b], wb[b]);
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (s0 + b < NS) acc[b] += ll_ok(wa[b], wb[b], tag) ? ll_val(wa[b], wb[b]) : ll_wait(row + 2 * b, tag);
+        if (s0 + b < NS) acc[b] += ll_val(wa[b], wb[b]);
     }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -421,8 +552,8 @@ __device__ __forceinline__ void ll_put_row(uint64_t* row, const double (&v)[(NS 
 // (relaxed arrival counters + LL rows: nobody waits for anybody's progress).  The final level
 // keeps its own octant in registers and loads the others all at once.
 template <int D, int NS = n_stats(D)>
-__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, uint32_t tag,
-                                          int lane) {
+__device__ __forceinline__ void finish_chunk_ll(const PassArgs& a, int64_t chunk, const double* chunk_sum,
+                                                uint32_t tag, int lane) {
   constexpr int K = (NS + 31) / 32;
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) ll_put(a.partials + (chunk * NS + st) * 2, chunk_sum[st], tag);
@@ -468,14 +599,23 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
       const int64_t h0 = lmax((int64_t)q * a.groups_per_octant, a.group_lo);
       const int64_t h1 = lmin(lmin((int64_t)(q + 1) * a.groups_per_octant, a.n_groups_total), a.group_lo + a.n_groups);
       live[q] = st < NS && q != o && q >= a.oct_lo && q < a.oct_hi && h1 > h0;
-      if (live[q]) ll_get2(a.opartials + (q * NS + st) * 2, wa[q], wb[q]);
+    }
+    unsigned long long t0 = 0;
+#pragma unroll 1
+    for (int tries = 0;; ++tries) {
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < kOctants; ++q)
+        if (live[q]) ll_get2(a.opartials + (q * NS + st) * 2, wa[q], wb[q]);
+#pragma unroll
+      for (int q = 0; q < kOctants; ++q)
+        if (live[q]) ok = ok && ll_ok(wa[q], wb[q], tag);
+      if (ok) break;
+      if (tries == 0) t0 = globaltimer_ns();
+      ll_check_deadline(t0);
     }
 #pragma unroll
-    for (int q = 0; q < kOctants; ++q)
-      v[q] = q == o ? osum[k]
-                    : (live[q] ? (ll_ok(wa[q], wb[q], tag) ? ll_val(wa[q], wb[q])
-                                                            : ll_wait(a.opartials + (q * NS + st) * 2, tag))
-                               : 0.0);
+    for (int q = 0; q < kOctants; ++q) v[q] = q == o ? osum[k] : (live[q] ? ll_val(wa[q], wb[q]) : 0.0);
 #pragma unroll
     for (int w = 1; w < kOctants; w *= 2)
 #pragma unroll
@@ -498,6 +638,15 @@ __device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, c
   }
   if (lane == 0) *a.pass_seq = tag + 1u;  // the next pass's tag (read after this grid completes)
   if (a.cta_trace && lane == 0) a.cta_trace[blockIdx.x * 8 + 6] = globaltimer_ns();
+}
+
+template <int D>
+__device__ __forceinline__ void finish_chunk(const PassArgs& a, int64_t chunk, const double* chunk_sum, uint32_t tag,
+                                          int lane) {
+  if constexpr (D <= CAVI_LL_MAX_D)
+    finish_chunk_ll<D>(a, chunk, chunk_sum, tag, lane);
+  else
+    finish_chunk_acqrel<D>(a, chunk, chunk_sum, lane);
 }
 
 // The sweep tail as its own one-warp kernel (tail.cuh): pairwise tree over the `world` shard
