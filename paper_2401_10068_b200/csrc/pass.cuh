@@ -732,6 +732,9 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 #ifndef CAVI_SEMI_Y_MAXD
 #define CAVI_SEMI_Y_MAXD 13  // d > CAVI_HYBRID_MAX_D: trailing Y columns in scalar up to this d (14, 15 spill)
 #endif
+#ifndef CAVI_SEMI_MAX_D
+#define CAVI_SEMI_MAX_D 14  // above: every G tile on the tensor cores, no per-lane trailing accumulators (N=16: 276 -> 285 sweeps/s; N=13-15 slower)
+#endif
 #ifndef CAVI_HYBRID_MAX_D
 #define CAVI_HYBRID_MAX_D 11  // largest d with the scalar trailing block (d = 12 spills: slower)
 #endif
@@ -752,7 +755,7 @@ struct MmaConsumer {
   static constexpr int NT = kHyb ? 1 : DP / 8;  // 8-wide output tiles on the tensor cores
   // d > CAVI_HYBRID_MAX_D: Y and the G tiles of rows < 8 on the tensor cores, the trailing
   // diagonal block of G (and g) as per-gene scalar FMAs instead of the 8x8 tile (1, 1)
-  static constexpr bool kSemi = D > 8 && !kHyb;
+  static constexpr bool kSemi = D > 8 && !kHyb && D <= CAVI_SEMI_MAX_D;
   static constexpr int RT = (kHyb || kSemi) ? D - 8 : 0;  // trailing dimensions done in scalar
   static constexpr int MTG = kSemi ? 1 : NT;              // G row tiles on the tensor cores
   // d > CAVI_HYBRID_MAX_D too: the trailing Y columns (k >= 8) as per-gene scalar FMAs with
