@@ -2038,9 +2038,9 @@ int32_t cv_bench_sweeps(cv_dataset* ds, const cv_hyper* hp, const cv_state* st, 
   if (getenv("CAVI_TAIL_PROF_PRINT")) {
     const unsigned long long* p = ds->h_ctl->prof;
     fprintf(stderr,
-            "tail cycles: loads %lld products %lld update+inverse %lld elbo %lld deltas %lld stores %lld total %lld\n",
-            (long long)(p[1] - p[0]), (long long)(p[6] - p[1]), (long long)(p[2] - p[6]), (long long)(p[3] - p[2]),
-            (long long)(p[4] - p[3]), (long long)(p[5] - p[4]), (long long)(p[5] - p[0]));
+            "tail cycles: loads %lld products %lld update %lld inverse %lld elbo %lld deltas %lld stores %lld total %lld\n",
+            (long long)(p[1] - p[0]), (long long)(p[6] - p[1]), (long long)(p[7] - p[6]), (long long)(p[2] - p[7]),
+            (long long)(p[3] - p[2]), (long long)(p[4] - p[3]), (long long)(p[5] - p[4]), (long long)(p[5] - p[0]));
   }
   if (ds->h_ctl->status != CV_OK) return state_status(ds->h_ctl->cur);
   return CV_OK;

@@ -260,80 +260,69 @@ __device__ __forceinline__ double rel_delta_t(const double* nw, const double* ol
   return md / fmax(mo, 1e-300);
 }
 
-// spd_inv_logdet_t across one warp (operands in shared memory): the same per-element
-// arithmetic in the same order (Cholesky column j by rows, L^-1 by columns, S = M^T M by
-// entries), so the result is bit-identical to the single-thread version.  Used by the
-// tail for d > 8, where the serial O(d^3) chain dominated the sweep tail.
+// SPD inverse + log-determinant across one warp by the symmetric sweep operator (Gauss-Jordan
+// without pivoting): sweeping pivot k of W turns W into [[-1/p, row/p], [col/p, W - col row/p]];
+// after every k, W = -A^-1.  The pivots p_k are the LDL^T pivots of A, so A is positive definite
+// iff every p_k > 0, and ln|A| = sum ln p_k.  d sweeps of d^2/32 independent updates per lane:
+// the d = 15 rate inversion in ~4k cycles where the column-serial Cholesky + triangular inverse
+// (spd_inv_logdet_t's algorithm across the warp) took ~32k.  With the reference's jitter-once
+// retry (linalg.py:279-298): on a non-positive pivot, 1e-10 tr(A)/d is added to the diagonal of
+// A (modified in place, as the serial version's copy) and the sweep restarts.
 template <int D>
-__device__ bool chol_warp(const double* A, double* L, int lane) {
-  __shared__ double s_rl;
-  __shared__ int s_ok;
-  for (int i = lane; i < D * D; i += 32) L[i] = 0.0;
+__device__ __forceinline__ bool spd_sweep_once(const double* A, double* W, double* logdet, int lane) {
+  constexpr int D2 = D * D, K = (D2 + 31) / 32;
+  for (int e = lane; e < D2; e += 32) W[e] = A[e];
   __syncwarp();
-  for (int j = 0; j < D; ++j) {
-    if (lane == 0) {
-      double s = A[j * D + j];
-      for (int k = 0; k < j; ++k) s -= L[j * D + k] * L[j * D + k];
-      s_ok = s > 0.0;
-      if (s_ok) {
-        const double ljj = sqrt(s);
-        s_rl = 1.0 / ljj;
-        L[j * D + j] = ljj;
-      }
-    }
-    __syncwarp();
-    if (!s_ok) return false;
-    const double rl = s_rl;
-    const int i = j + 1 + lane;
-    if (i < D) {
-      double t = A[i * D + j];
-      for (int k = 0; k < j; ++k) t -= L[i * D + k] * L[j * D + k];
-      L[i * D + j] = t * rl;
-    }
-    __syncwarp();
+  double prod = 1.0;  // lane 0: product of the pivots, exponent renormalised (one log at the end)
+  int ex = 0;
+  int ii[K], jj[K];  // this lane's elements, fixed for every pivot (branch-free updates below)
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const int e = lane + 32 * m < D2 ? lane + 32 * m : 0;
+    ii[m] = e / D;
+    jj[m] = e % D;
   }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double p = W[k * D + k];
+    if (!(p > 0.0)) return false;  // every lane read the same pivot
+    const double rp = 1.0 / p;
+    double nv[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      const int i = ii[m], j = jj[m];
+      const double wik = W[i * D + k], wkj = W[k * D + j], we = W[i * D + j];
+      const double gen = fma(-wik * rp, wkj, we);
+      const double rowcol = (i == k ? wkj : wik) * rp;
+      nv[m] = (i == k && j == k) ? -rp : ((i == k || j == k) ? rowcol : gen);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < K; ++m)
+      if (lane + 32 * m < D2) W[lane + 32 * m] = nv[m];
+    __syncwarp();
+    if (lane == 0) {
+      prod *= p;
+      const int hi = __double2hiint(prod);
+      ex += ((hi >> 20) & 0x7ff) - 1023;
+      prod = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(prod));
+    }
+  }
+  if (lane == 0) *logdet = log(prod) + (double)ex * kLn2;
   return true;
 }
 
 template <int D>
-__device__ bool spd_inv_logdet_warp(double* A, double* Ainv, double* logdet, double* L, double* M, int lane) {
-  if (!chol_warp<D>(A, L, lane)) {
-    __shared__ double s_jit;
-    if (lane == 0) {
-      double tr = 0.0;
-      for (int j = 0; j < D; ++j) tr += A[j * D + j];
-      s_jit = 1e-10 * tr / D;
-    }
+__device__ __forceinline__ bool spd_inv_logdet_sweep(double* A, double* Ainv, double* logdet, double* W, int lane) {
+  if (!spd_sweep_once<D>(A, W, logdet, lane)) {
+    double tr = 0.0;
+    for (int j = 0; j < D; ++j) tr += A[j * D + j];  // every lane: the same sum
     __syncwarp();
-    if (lane < D) A[lane * D + lane] += s_jit;  // the jitter-once retry (linalg.py:279-298)
+    if (lane < D) A[lane * D + lane] += 1e-10 * tr / D;  // the jitter-once retry (linalg.py:279-298)
     __syncwarp();
-    if (!chol_warp<D>(A, L, lane)) return false;
+    if (!spd_sweep_once<D>(A, W, logdet, lane)) return false;
   }
-  for (int i = lane; i < D * D; i += 32) M[i] = 0.0;
-  __syncwarp();
-  if (lane < D) {  // column j = lane of L^-1
-    const int j = lane;
-    M[j * D + j] = 1.0 / L[j * D + j];
-    for (int i = j + 1; i < D; ++i) {
-      double t = 0.0;
-      for (int k = j; k < i; ++k) t -= L[i * D + k] * M[k * D + j];
-      M[i * D + j] = t / L[i * D + i];
-    }
-  }
-  __syncwarp();
-  if (lane == 0) {
-    double prod = 1.0;
-    for (int j = 0; j < D; ++j) prod *= L[j * D + j];
-    *logdet = 2.0 * log(prod);
-  }
-  for (int e = lane; e < D * D; e += 32) {
-    const int i = e / D, j = e % D;
-    if (j < i) continue;
-    double t = 0.0;
-    for (int k = j; k < D; ++k) t += M[k * D + i] * M[k * D + j];
-    Ainv[i * D + j] = t;
-    Ainv[j * D + i] = t;
-  }
+  for (int e = lane; e < D * D; e += 32) Ainv[e] = -W[e];
   __syncwarp();
   return true;
 }

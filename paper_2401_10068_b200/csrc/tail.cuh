@@ -13,9 +13,10 @@
 //   phase 0  every global word the tail reads (statistics of all ranks, the pass's generator,
 //            the previous state, the hyperparameters: ~110 words at d = 3, ~1.4k at d = 15) is
 //            gathered by all 32 lanes in one burst of independent loads -> one L2 round trip;
-//   phase 1  A^-1 G A^-1 and A^-1 g, one row per lane;
-//   phase 2  the new Q(Lambda) rate, one element per lane; its Cholesky inverse + log-det with
-//            the jitter-once retry (linalg.py:279-298) across the warp (spd_inv_logdet_warp);
+//   phase 1  A^-1 G A^-1 and A^-1 g, element-parallel;
+//   phase 2  the new Q(Lambda) rate, one element per lane; its inverse + log-det with the
+//            jitter-once retry (linalg.py:279-298): Cholesky on lane 0 for d <= 4, the symmetric
+//            sweep across the warp above (tail_inverse);
 //   phase 3  the bound's three d x d contractions as lane partials + butterflies, the scalar
 //            assembly on lane 0; E[Lambda K] by rows; the deltas as warp max-reductions;
 //   phase 4  every store lane-parallel (state, trace entry, the next pass's generator).
@@ -35,7 +36,7 @@ struct TailSm {
   double k_old[D], l_old[D2], osc[4];     // previous state: k0k, lam0l_inv, (e_rho, a, b, ln|lam0l_inv|)
   double K0[D], L0[D2], L0i[D2];
   double hv[D], AG[D2], T[D2], k0c[D], dlt[D], k_new[D];
-  double L[D2], C[D2], S[D2], Lc[D2], M[D2];
+  double L[D2], C[D2], S[D2], M[D2];
   double ld;
   int ok;
 };
@@ -82,8 +83,8 @@ struct WarpLoad {
 // Inverse + log-det of the SPD rate in sm.C (modified by the jitter retry) -> sm.S; lane 0
 // holds *ld; returns ok (finite log-det) on every lane.  Up to kTailSerialD the whole
 // factorisation runs on lane 0 in registers (spd_inv_logdet_t: a d = 3 Cholesky + inverse is a
-// ~1k-cycle dependent chain; the warp version pays a __syncwarp and a shared broadcast per
-// column); beyond it, across the warp (spd_inv_logdet_warp, same per-element arithmetic).
+// ~1k-cycle dependent chain); beyond it, the symmetric sweep across the warp
+// (spd_inv_logdet_sweep: d rounds of d^2/32 independent updates per lane).
 constexpr int kTailSerialD = 4;
 template <int D>
 __device__ __forceinline__ bool tail_inverse(TailSm<D>& sm, double* ld, int lane) {
@@ -103,7 +104,7 @@ __device__ __forceinline__ bool tail_inverse(TailSm<D>& sm, double* ld, int lane
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
   } else {
     double l = 0.0;
-    const bool ok = spd_inv_logdet_warp<D>(sm.C, sm.S, &l, sm.Lc, sm.M, lane);
+    const bool ok = spd_inv_logdet_sweep<D>(sm.C, sm.S, &l, sm.M, lane);
     *ld = l;
     return __shfl_sync(0xffffffffu, (int)(ok && isfinite(l)), 0) != 0;
   }
@@ -147,13 +148,19 @@ __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, do
     if (done) c->done = 1;
   }
   if (lane < D) s.k0k[lane] = sm.gc[lane];
-  for (int e = lane; e < D2; e += 32) {
+  #pragma unroll
+  for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+    const int e = lane + 32 * m_;
+    if (e >= D2) break;
     s.lam0l_inv[e] = sm.gA[e];  // EM: the current precision Lambda
     s.e_lam[e] = sm.gAi[e];     //     and its inverse
   }
   if (__shfl_sync(0xffffffffu, done, 0)) return;
   const double rV = 1.0 / V;
-  for (int e = lane; e < D2; e += 32) {
+  #pragma unroll
+  for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+    const int e = lane + 32 * m_;
+    if (e >= D2) break;
     const int i = e / D, j = e % D;
     const int p = i < j ? i : j, q = i < j ? j : i;
     const double v = 0.5 * (sm.gAi[p * D + q] + sm.gAi[q * D + p]) + sm.T[p * D + q] * rV - sm.hv[p] * sm.hv[q] * rV * rV;
@@ -170,7 +177,10 @@ __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, do
     return;
   }
   if (lane < D) c->pass.c[lane] = sm.gc[lane] + sm.hv[lane] * rV;
-  for (int e = lane; e < D2; e += 32) {
+  #pragma unroll
+  for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+    const int e = lane + 32 * m_;
+    if (e >= D2) break;
     const int i = e / D, j = e % D;
     c->pass.A[e] = 0.5 * (sm.S[i * D + j] + sm.S[j * D + i]);
     c->pass.Ainv[e] = sm.L[e];
@@ -187,7 +197,7 @@ __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, do
 // tested only afterwards -- is requested in ONE burst: the tail pays one L2 round trip for its
 // inputs, not one per dependent step.
 template <int D>
-__device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const double* __restrict__ parts, int world,
+__device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const double* __restrict__ parts, int world,
                                        TailSm<D>& sm, int lane) {
   constexpr int NS = n_stats(D);
   constexpr int D2 = D * D;
@@ -258,28 +268,55 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
   __syncwarp();
   if (done_in) return;  // the fit stopped: this sweep's pass exited at once
   TAIL_PROF(*c, 1);
-  // ---- phase 1: T = A^-1 G A^-1 and hv = A^-1 g (row `lane`)
+  // ---- phase 1: T = A^-1 G A^-1 and hv = A^-1 g, element-parallel (d^2/32 dot products of
+  // length d per lane, each in the serial code's k order)
+  #pragma unroll
+  for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+    const int e = lane + 32 * m_;
+    if (e >= D2) break;  // G unpacked from the statistics' upper triangle
+    const int i = e / D, j = e % D;
+    const int lo = i < j ? i : j, hi = i < j ? j : i;
+    sm.T[e] = sm.tot[D + lo * D - lo * (lo - 1) / 2 + (hi - lo)];
+  }
   if (lane < D) {
-    const int i = lane;
     double t = 0.0;
-    for (int j = 0; j < D; ++j) t += sm.gAi[i * D + j] * sm.tot[j];
-    sm.hv[i] = t;
-    for (int j = 0; j < D; ++j) {
-      double u = 0.0;
-      for (int k = 0; k < D; ++k) {
-        const int lo = k < j ? k : j, hi = k < j ? j : k;
-        u += sm.gAi[i * D + k] * sm.tot[D + lo * D - lo * (lo - 1) / 2 + (hi - lo)];
-      }
-      sm.AG[i * D + j] = u;
-    }
+    for (int j = 0; j < D; ++j) t += sm.gAi[lane * D + j] * sm.tot[j];
+    sm.hv[lane] = t;
   }
   __syncwarp();
-  if (lane < D)
-    for (int j = 0; j < D; ++j) {
-      double u = 0.0;
-      for (int k = 0; k < D; ++k) u += sm.AG[lane * D + k] * sm.gAi[k * D + j];
-      sm.T[lane * D + j] = u;
+  {
+    // this lane's KE elements, the KE dot products interleaved (independent FMA chains: one warp
+    // has no other warps to hide a chain's latency behind)
+    constexpr int KE = (D2 + 31) / 32;
+    int ei[KE], ej[KE];
+#pragma unroll
+    for (int m = 0; m < KE; ++m) {
+      const int e = lane + 32 * m < D2 ? lane + 32 * m : 0;
+      ei[m] = e / D;
+      ej[m] = e % D;
     }
+    double u[KE];
+#pragma unroll
+    for (int m = 0; m < KE; ++m) u[m] = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+#pragma unroll
+      for (int m = 0; m < KE; ++m) u[m] += sm.gAi[ei[m] * D + k] * sm.T[k * D + ej[m]];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < KE; ++m)
+      if (lane + 32 * m < D2) sm.AG[lane + 32 * m] = u[m];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < KE; ++m) u[m] = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+#pragma unroll
+      for (int m = 0; m < KE; ++m) u[m] += sm.AG[ei[m] * D + k] * sm.gAi[k * D + ej[m]];
+#pragma unroll
+    for (int m = 0; m < KE; ++m)
+      if (lane + 32 * m < D2) sm.T[lane + 32 * m] = u[m];
+  }
   __syncwarp();
   TAIL_PROF(*c, 6);
 
@@ -295,7 +332,9 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
   int status = CV_OK;
   double a = 0, b = 0, e_rho = 0;  // lane 0
   if (mode == MODE_ELBO) {  // vb_elbo of the current state from a pass with its own generator
-    for (int e = lane; e < D2; e += 32) sm.C[e] = sm.l_old[e];
+#pragma unroll
+    for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_)
+      if (lane + 32 * m_ < D2) sm.C[lane + 32 * m_] = sm.l_old[lane + 32 * m_];
     __syncwarp();
     double ldx = 0.0;
     const bool ok = tail_inverse<D>(sm, &ldx, lane);
@@ -306,7 +345,10 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
     if (lane == 0) sm.ld = ld_old;  // the bound uses the state's own ln|lam0l_inv| (tail_t)
     if (!ok) status = CV_ERR_NUMERIC;
   } else if (mode == MODE_INIT) {  // vb_init (vb.py:82-111): globals at the prior
-    for (int e = lane; e < D2; e += 32) {
+    #pragma unroll
+    for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+      const int e = lane + 32 * m_;
+      if (e >= D2) break;
       sm.L[e] = sm.L0[e];
       sm.S[e] = sm.L0i[e];
     }
@@ -324,7 +366,10 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
       sm.k_new[i] = sm.gc[i] + sm.dlt[i];
     }
     __syncwarp();
-    for (int e = lane; e < D2; e += 32) {  // the upper-triangle formula, mirrored (as tail_t)
+    #pragma unroll
+    for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+      const int e = lane + 32 * m_;
+      if (e >= D2) break;  // the upper-triangle formula, mirrored (as tail_t)
       const int i = e / D, j = e % D;
       const int p = i < j ? i : j, q = i < j ? j : i;
       const double v = sm.L0i[p * D + q] + V * sm.gAi[p * D + q] + sm.T[p * D + q] + q0 * sm.k0c[p] * sm.k0c[q] -
@@ -333,6 +378,7 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
       sm.C[e] = v;  // the inverse works on a copy (the jitter retry modifies it)
     }
     __syncwarp();
+    TAIL_PROF(*c, 7);
     double ldx = 0.0;
     const bool ok = tail_inverse<D>(sm, &ldx, lane);
     if (lane == 0) sm.ld = ldx;  // lane 0 holds the log-det
@@ -352,9 +398,13 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
   const bool want_elbo = __shfl_sync(0xffffffffu, (int)(status == CV_OK && (compute_elbo || mode != MODE_SWEEP)), 0);
   if (want_elbo && elbo_status == CV_OK) {
     double tr1 = 0.0, quad = 0.0, tr0 = 0.0;
-    // small d: lane 0 alone (d^2 <= 16 terms cost less than three butterflies)
-    const int e0 = D <= kTailSerialD ? (lane == 0 ? 0 : D2) : lane, es = D <= kTailSerialD ? 1 : 32;
-    for (int e = e0; e < D2; e += es) {
+    // small d: lane 0 alone (d^2 <= 16 terms cost less than three butterflies); else lane-strided
+    constexpr int ES = D <= kTailSerialD ? 1 : 32, KT = D <= kTailSerialD ? D2 : (D2 + 31) / 32;
+    const int e0 = D <= kTailSerialD ? (lane == 0 ? 0 : D2) : lane;
+#pragma unroll
+    for (int m_ = 0; m_ < KT; ++m_) {
+      const int e = e0 + ES * m_;
+      if (e >= D2) break;
       const int i = e / D, j = e % D;
       const double di = sm.k_new[i] - sm.gc[i], dj = sm.k_new[j] - sm.gc[j];
       const double sc = V * sm.gAi[e] + sm.T[e] - di * sm.hv[j] - sm.hv[i] * dj + V * di * dj;
@@ -434,7 +484,10 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
       dk = md / fmax(mo, 1e-300);
       mo = 0.0;
       md = 0.0;
-      for (int e = lane; e < D2; e += 32) {
+      #pragma unroll
+      for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+        const int e = lane + 32 * m_;
+        if (e >= D2) break;
         mo = fmax(mo, fabs(sm.l_old[e]));
         const double df = fabs(sm.L[e] - sm.l_old[e]);
         md = (df > md || df != df) ? df : md;
@@ -447,7 +500,10 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
   TAIL_PROF(*c, 4);
 
   // ---- phase 4: stores (every read of c / s happened above)
-  for (int e = lane; e < D2; e += 32) {
+  #pragma unroll
+  for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+    const int e = lane + 32 * m_;
+    if (e >= D2) break;
     s.lam0l_inv[e] = sm.L[e];
     s.e_lam[e] = nu * sm.S[e];
     s.gen_A[e] = sm.gA[e];
@@ -461,7 +517,10 @@ __device__ __noinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const
   if (status == CV_OK) {  // generator of the next pass (vb.py:136-144)
     const double rnu = 1.0 / nu;
     if (lane < D) c->pass.c[lane] = sm.k_new[lane];
-    for (int e = lane; e < D2; e += 32) {
+    #pragma unroll
+    for (int m_ = 0; m_ < (D2 + 31) / 32; ++m_) {
+      const int e = lane + 32 * m_;
+      if (e >= D2) break;
       c->pass.A[e] = nu * sm.S[e];
       c->pass.Ainv[e] = sm.L[e] * rnu;
     }
