@@ -47,7 +47,8 @@ enum {
   CV_ERR_CUDA = 4,
   CV_ERR_IMPROPER = 5, /* NumericError("Q(Lambda) is improper; dataset too small") */
   CV_ERR_FORMAT = 6,   /* cli.UsageError: malformed dataset file (header / field count) */
-  CV_ERR_PEER = 7      /* multi-GPU: a peer's statistics did not arrive within CAVI_PEER_TIMEOUT_S */
+  CV_ERR_PEER = 7,     /* multi-GPU: a peer's statistics did not arrive within CAVI_PEER_TIMEOUT_S */
+  CV_ERR_SINGULAR = 8  /* linalg.BatchItemError: a d <= 3 item with |det| < 1e-300 (vb_init's Lambda0) */
 };
 
 /* storage layouts of the measurement stream in HBM */
@@ -246,6 +247,12 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
                             int64_t V, double a_rho, double b_rho, const double* k0k, const double* lam0l_inv,
                             int64_t n, int32_t device, double* K_out, double* Lam_out, double* rho_out,
                             uint64_t* block_end);
+
+/* test hook: the sweep tail's rate inversion (the reference's inverse_batched semantics --
+ * adjugate with the |det| >= 1e-300 guard for d <= 3, pivoted elimination above -- with the
+ * jitter-once retry) on one d x d matrix on `device`: *ok = 0 where the reference raises
+ * NumericError after the retry; *logdet = ln|det| of the matrix inverted. */
+int32_t cv_test_rate_inverse(const double* A, int32_t d, int32_t device, double* Ainv, double* logdet, int32_t* ok);
 
 /* ---- pinned host memory (for end-to-end uploads at DMA speed) --------- */
 int32_t cv_host_alloc(int64_t bytes, void** out);

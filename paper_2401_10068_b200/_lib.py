@@ -16,7 +16,7 @@ from . import linalg
 MAX_D = 15
 MAX_D2 = MAX_D * MAX_D
 
-OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT, ERR_PEER = range(8)
+OK, ERR_NUMERIC, ERR_NONFINITE, ERR_ARG, ERR_CUDA, ERR_IMPROPER, ERR_FORMAT, ERR_PEER, ERR_SINGULAR = range(9)
 STORE_F64, STORE_F32, STORE_F32M = 0, 1, 2
 
 _LIB_PATH = os.environ.get("CAVI_LIB", os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcavi.so"))
@@ -114,6 +114,7 @@ _SIGS = {
     "cv_posterior_sample": (C.c_int32, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_double,
                                         C.c_int64, C.c_double, C.c_double, _D, _D, C.c_int64, C.c_int32, _D, _D, _D,
                                         _P(C.c_uint64)]),
+    "cv_test_rate_inverse": (C.c_int32, [_D, C.c_int32, C.c_int32, _D, _D, _P(C.c_int32)]),
     "cv_host_alloc": (C.c_int32, [C.c_int64, _P(C.c_void_p)]),
     "cv_host_free": (None, [C.c_void_p]),
     "cv_bench_sweeps": (C.c_int32, [C.c_void_p, _P(CvHyper), _P(CvState), C.c_int32, C.c_int32, _D, _D,
@@ -156,11 +157,14 @@ class PeerTimeoutError(RuntimeError):
     (a stalled or failed rank).  The next shard call resyncs the communicator."""
 
 
-def check(rc: int) -> None:
-    """Map a status code to the reference's exception types (linalg.py:46-69)."""
+def check(rc: int, n_items: int | None = None) -> None:
+    """Map a status code to the reference's exception types (linalg.py:46-69).  n_items: the
+    batch a singular-item error refers to (vb_init's V per-gene precisions, vb.py:94-96)."""
     if rc == OK:
         return
     msg = lib().cv_last_error().decode(errors="replace")
+    if rc == ERR_SINGULAR:  # BatchItemError(msg, every item): the reference's exact message
+        raise linalg.BatchItemError(msg, [np.int64(i) for i in range(n_items or 0)])
     if rc in (ERR_NUMERIC, ERR_IMPROPER):
         raise linalg.NumericError(msg)
     if rc == ERR_NONFINITE:

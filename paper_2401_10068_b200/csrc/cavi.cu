@@ -483,6 +483,7 @@ int upload_hyper(cv_dataset* ds, const cv_hyper* hp) {
   int st = 0;
   CK(cudaMemcpyAsync(&st, &ds->hyp->setup_status, sizeof st, cudaMemcpyDeviceToHost, ds->stream));
   CK(cudaStreamSynchronize(ds->stream));
+  if (st == CV_ERR_SINGULAR) return fail(CV_ERR_SINGULAR, "singular %dx%d item", h.d, h.d);
   if (st != CV_OK) return fail(CV_ERR_NUMERIC, "Lambda0 is not positive definite");
   if (ds->bad_input & 1) return fail(CV_ERR_NONFINITE, "non-finite values in A");
   return CV_OK;
@@ -1942,6 +1943,26 @@ int32_t cv_posterior_sample(uint64_t seed, uint64_t stream_id, uint64_t block0, 
   CK(cudaStreamSynchronize(st));
   if (pst != CV_OK) return fail(CV_ERR_NUMERIC, "non-positive pivot in the Q(Lambda) scale");
   *block_end = block;
+  return CV_OK;
+}
+
+int32_t cv_test_rate_inverse(const double* A, int32_t d, int32_t device, double* Ainv, double* logdet, int32_t* ok) {
+  if (!A || !Ainv || !logdet || !ok) return fail(CV_ERR_ARG, "null pointer");
+  if (d < 1 || d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported", d);
+  PassKernel pk = pass_for(d, CV_STORE_F64);
+  CK(cudaSetDevice(device));
+  CallScratch sc;
+  double* buf = nullptr;
+  int* dok = nullptr;
+  CK(sc.alloc(&buf, sizeof(double) * (2 * d * d + 1)));
+  CK(sc.alloc(&dok, sizeof(int)));
+  CK(cudaMemcpy(buf, A, sizeof(double) * d * d, cudaMemcpyHostToDevice));
+  pk.rate_inverse_test<<<1, 32>>>(buf, buf + d * d, buf + 2 * d * d, dok);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(Ainv, buf + d * d, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(logdet, buf + 2 * d * d, sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(ok, dok, sizeof(int), cudaMemcpyDeviceToHost));
   return CV_OK;
 }
 

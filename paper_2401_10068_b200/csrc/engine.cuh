@@ -154,9 +154,10 @@ __device__ __forceinline__ bool chol_t(const double* A, double* L) {
   return true;
 }
 
-// inverse + log-determinant of an SPD matrix; false if not PD after the retry
+// inverse + log-determinant of an SPD matrix by Cholesky; false if not PD after the retry
+// (the posterior sampler's covariance, where a factor is needed anyway)
 template <int D>
-__device__ __forceinline__ bool spd_inv_logdet_t(const double* A, double* Ainv, double* logdet) {
+__device__ __forceinline__ bool spd_inv_logdet_chol_t(const double* A, double* Ainv, double* logdet) {
   double L[D * D];
   if (!chol_t<D>(A, L)) {
     double tr = 0.0;
@@ -198,6 +199,116 @@ __device__ __forceinline__ bool spd_inv_logdet_t(const double* A, double* Ainv, 
       Ainv[j * D + i] = t;
     }
   return isfinite(*logdet);
+}
+
+// The reference's batched inverse (linalg.py:111-192) on one matrix, for the rate / precision
+// inversions the sweep and the bound perform (vb.py:137, 183, 216-304; em.py:84-93):
+//   d <= 3  closed-form adjugate times 1/det, cofactor by cofactor as _inv2 / _inv3, "singular"
+//           when |det| < 1e-300 (DET_GUARD);
+//   d >= 4  elimination with partial pivoting (LAPACK getrf/getri's algorithm class), "singular"
+//           only on an exactly zero pivot (LinAlgError).
+// No positive-definiteness test: like the reference, an indefinite but non-singular matrix is
+// inverted.  *logdet = ln|det| (the reference's slogdet, sign dropped).
+template <int D>
+__device__ __forceinline__ bool ref_inv_once_t(const double* A, double* Ainv, double* logabs) {
+  if constexpr (D == 1) {
+    if (!(fabs(A[0]) >= 1e-300)) return false;
+    Ainv[0] = 1.0 / A[0];
+    *logabs = log(fabs(A[0]));
+    return true;
+  } else if constexpr (D == 2) {
+    const double a = A[0], b = A[1], c = A[2], d = A[3];
+    const double det = a * d - b * c;
+    if (!(fabs(det) >= 1e-300)) return false;
+    const double r = 1.0 / det;
+    Ainv[0] = d * r;
+    Ainv[1] = -b * r;
+    Ainv[2] = -c * r;
+    Ainv[3] = a * r;
+    *logabs = log(fabs(det));
+    return true;
+  } else if constexpr (D == 3) {
+    auto m = [&](int i, int j) { return A[i * 3 + j]; };
+    const double c00 = m(1, 1) * m(2, 2) - m(1, 2) * m(2, 1);
+    const double c01 = m(1, 2) * m(2, 0) - m(1, 0) * m(2, 2);
+    const double c02 = m(1, 0) * m(2, 1) - m(1, 1) * m(2, 0);
+    const double det = m(0, 0) * c00 + m(0, 1) * c01 + m(0, 2) * c02;
+    if (!(fabs(det) >= 1e-300)) return false;
+    const double c10 = m(0, 2) * m(2, 1) - m(0, 1) * m(2, 2);
+    const double c11 = m(0, 0) * m(2, 2) - m(0, 2) * m(2, 0);
+    const double c12 = m(0, 1) * m(2, 0) - m(0, 0) * m(2, 1);
+    const double c20 = m(0, 1) * m(1, 2) - m(0, 2) * m(1, 1);
+    const double c21 = m(0, 2) * m(1, 0) - m(0, 0) * m(1, 2);
+    const double c22 = m(0, 0) * m(1, 1) - m(0, 1) * m(1, 0);
+    const double r = 1.0 / det;
+    Ainv[0] = c00 * r;
+    Ainv[1] = c10 * r;
+    Ainv[2] = c20 * r;
+    Ainv[3] = c01 * r;
+    Ainv[4] = c11 * r;
+    Ainv[5] = c21 * r;
+    Ainv[6] = c02 * r;
+    Ainv[7] = c12 * r;
+    Ainv[8] = c22 * r;
+    *logabs = log(fabs(det));
+    return true;
+  } else {
+    // Gauss-Jordan with partial pivoting on [A | I] (one thread; the batched kernel's d >= 4)
+    double M[D * 2 * D];
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < 2 * D; ++j) M[i * 2 * D + j] = j < D ? A[i * D + j] : (j - D == i ? 1.0 : 0.0);
+    double prod = 1.0;
+    int ex = 0;
+    for (int k = 0; k < D; ++k) {
+      int p = k;
+      for (int i = k + 1; i < D; ++i)
+        if (fabs(M[i * 2 * D + k]) > fabs(M[p * 2 * D + k])) p = i;
+      const double piv = M[p * 2 * D + k];
+      if (piv == 0.0) return false;
+      if (p != k)
+        for (int j = 0; j < 2 * D; ++j) {
+          const double t = M[k * 2 * D + j];
+          M[k * 2 * D + j] = M[p * 2 * D + j];
+          M[p * 2 * D + j] = t;
+        }
+      const double rp = 1.0 / piv;
+      for (int j = 0; j < 2 * D; ++j) M[k * 2 * D + j] *= rp;
+      for (int i = 0; i < D; ++i) {
+        if (i == k) continue;
+        const double f = M[i * 2 * D + k];
+        for (int j = 0; j < 2 * D; ++j) M[i * 2 * D + j] = fma(-f, M[k * 2 * D + j], M[i * 2 * D + j]);
+      }
+      prod *= fabs(piv);
+      const int hi = __double2hiint(prod);
+      ex += ((hi >> 20) & 0x7ff) - 1023;
+      prod = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(prod));
+    }
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < D; ++j) Ainv[i * D + j] = M[i * 2 * D + D + j];
+    *logabs = log(prod) + (double)ex * kLn2;
+    return true;
+  }
+}
+
+// ref_inv_once_t with the jitter-once retry (linalg.py:279-298); *logdet = ln|det| of the
+// matrix actually inverted.  False: singular after the retry (NumericError).
+template <int D>
+__device__ __forceinline__ bool spd_inv_logdet_t(const double* A, double* Ainv, double* logdet) {
+  double ld = 0.0;
+  if (!ref_inv_once_t<D>(A, Ainv, &ld)) {
+    double tr = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) tr += A[j * D + j];
+    const double jit = 1e-10 * tr / D;
+    double J[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) J[i] = A[i];
+#pragma unroll
+    for (int j = 0; j < D; ++j) J[j * D + j] += jit;
+    if (!ref_inv_once_t<D>(J, Ainv, &ld)) return false;
+  }
+  *logdet = ld;
+  return isfinite(ld);
 }
 
 // runtime-d variant, used once per call by the setup kernel (workspaces in Hyp)
@@ -260,77 +371,101 @@ __device__ __forceinline__ double rel_delta_t(const double* nw, const double* ol
   return md / fmax(mo, 1e-300);
 }
 
-// SPD inverse + log-determinant across one warp by the symmetric sweep operator (Gauss-Jordan
-// without pivoting): sweeping pivot k of W turns W into [[-1/p, row/p], [col/p, W - col row/p]];
-// after every k, W = -A^-1.  The pivots p_k are the LDL^T pivots of A, so A is positive definite
-// iff every p_k > 0, and ln|A| = sum ln p_k.  d sweeps of d^2/32 independent updates per lane:
-// the d = 15 rate inversion in ~4k cycles where the column-serial Cholesky + triangular inverse
-// (spd_inv_logdet_t's algorithm across the warp) took ~32k.  With the reference's jitter-once
-// retry (linalg.py:279-298): on a non-positive pivot, 1e-10 tr(A)/d is added to the diagonal of
-// A (modified in place, as the serial version's copy) and the sweep restarts.
+// ref_inv_once_t's d >= 4 branch across one warp: Gauss-Jordan with partial pivoting on
+// [A | I] (2 d^2 / 32 elements per lane per pivot; the pivot search a warp argmax with the lowest
+// row on ties, as idamax).  "Singular" only on an exactly zero pivot, like LAPACK's getrf.
 template <int D>
-__device__ __forceinline__ bool spd_sweep_once(const double* A, double* W, double* logdet, int lane) {
-  constexpr int D2 = D * D, K = (D2 + 31) / 32;
-  for (int e = lane; e < D2; e += 32) W[e] = A[e];
+__device__ bool ref_inv_once_warp(const double* A, double* M, double* Ainv, double* logabs, int lane) {
+  constexpr int W = 2 * D, N = D * W, K = (N + 31) / 32;
+  for (int e = lane; e < N; e += 32) {
+    const int i = e / W, j = e % W;
+    M[e] = j < D ? A[i * D + j] : (j - D == i ? 1.0 : 0.0);
+  }
   __syncwarp();
-  double prod = 1.0;  // lane 0: product of the pivots, exponent renormalised (one log at the end)
-  int ex = 0;
-  int ii[K], jj[K];  // this lane's elements, fixed for every pivot (branch-free updates below)
+  int ei[K], ej[K];
 #pragma unroll
   for (int m = 0; m < K; ++m) {
-    const int e = lane + 32 * m < D2 ? lane + 32 * m : 0;
-    ii[m] = e / D;
-    jj[m] = e % D;
+    const int e = lane + 32 * m < N ? lane + 32 * m : 0;
+    ei[m] = e / W;
+    ej[m] = e % W;
   }
-#pragma unroll
+  double prod = 1.0;  // lane 0: product of |pivots|, exponent renormalised
+  int ex = 0;
+#pragma unroll 1
   for (int k = 0; k < D; ++k) {
-    const double p = W[k * D + k];
-    if (!(p > 0.0)) return false;  // every lane read the same pivot
-    const double rp = 1.0 / p;
+    double v = (lane >= k && lane < D) ? fabs(M[lane * W + k]) : -1.0;
+    int p = lane;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+      const int op = __shfl_xor_sync(0xffffffffu, p, off);
+      if (ov > v || (ov == v && op < p)) {
+        v = ov;
+        p = op;
+      }
+    }
+    const double piv = M[p * W + k];
+    if (piv == 0.0) return false;  // every lane has the same p
+    if (p != k) {
+      for (int j = lane; j < W; j += 32) {
+        const double t = M[k * W + j];
+        M[k * W + j] = M[p * W + j];
+        M[p * W + j] = t;
+      }
+      __syncwarp();
+    }
+    const double rp = 1.0 / piv;
     double nv[K];
 #pragma unroll
     for (int m = 0; m < K; ++m) {
-      const int i = ii[m], j = jj[m];
-      const double wik = W[i * D + k], wkj = W[k * D + j], we = W[i * D + j];
-      const double gen = fma(-wik * rp, wkj, we);
-      const double rowcol = (i == k ? wkj : wik) * rp;
-      nv[m] = (i == k && j == k) ? -rp : ((i == k || j == k) ? rowcol : gen);
+      const int i = ei[m], j = ej[m];
+      const double mkj = M[k * W + j] * rp;
+      nv[m] = i == k ? mkj : fma(-M[i * W + k], mkj, M[i * W + j]);
     }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < K; ++m)
-      if (lane + 32 * m < D2) W[lane + 32 * m] = nv[m];
+      if (lane + 32 * m < N) M[lane + 32 * m] = nv[m];
     __syncwarp();
     if (lane == 0) {
-      prod *= p;
+      prod *= fabs(piv);
       const int hi = __double2hiint(prod);
       ex += ((hi >> 20) & 0x7ff) - 1023;
       prod = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(prod));
     }
   }
-  if (lane == 0) *logdet = log(prod) + (double)ex * kLn2;
+  for (int e = lane; e < D * D; e += 32) Ainv[e] = M[(e / D) * W + D + e % D];
+  if (lane == 0) *logabs = log(prod) + (double)ex * kLn2;
+  __syncwarp();
   return true;
 }
 
+// ... with the jitter-once retry (linalg.py:279-298) on a jittered copy of A (A unchanged)
 template <int D>
-__device__ __forceinline__ bool spd_inv_logdet_sweep(double* A, double* Ainv, double* logdet, double* W, int lane) {
-  if (!spd_sweep_once<D>(A, W, logdet, lane)) {
-    double tr = 0.0;
-    for (int j = 0; j < D; ++j) tr += A[j * D + j];  // every lane: the same sum
-    __syncwarp();
-    if (lane < D) A[lane * D + lane] += 1e-10 * tr / D;  // the jitter-once retry (linalg.py:279-298)
-    __syncwarp();
-    if (!spd_sweep_once<D>(A, W, logdet, lane)) return false;
-  }
-  for (int e = lane; e < D * D; e += 32) Ainv[e] = -W[e];
+__device__ bool ref_inv_logdet_warp(const double* A, double* J, double* M, double* Ainv, double* logdet, int lane) {
+  if (ref_inv_once_warp<D>(A, M, Ainv, logdet, lane)) return true;
+  double tr = 0.0;
+  for (int j = 0; j < D; ++j) tr += A[j * D + j];  // every lane: the same sum
+  for (int e = lane; e < D * D; e += 32) J[e] = A[e] + ((e / D == e % D) ? 1e-10 * tr / D : 0.0);
   __syncwarp();
-  return true;
+  return ref_inv_once_warp<D>(J, M, Ainv, logdet, lane);
 }
 
 // ------------------------------------------------------------------ setup of the constants
 static __device__ __noinline__ void hyp_setup(Hyp& h) {
   const int d = h.d;
   h.setup_status = CV_OK;
+  if (d <= 3) {  // vb_init inverts Lambda0 per gene by the adjugate (vb.py:94-97, linalg.py:111-153): its guard
+    const double* A = h.L0;
+    const double det = d == 1 ? A[0]
+                       : d == 2 ? A[0] * A[3] - A[1] * A[2]
+                                : A[0] * (A[4] * A[8] - A[5] * A[7]) + A[1] * (A[5] * A[6] - A[3] * A[8]) +
+                                      A[2] * (A[3] * A[7] - A[4] * A[6]);
+    if (!(fabs(det) >= 1e-300)) {
+      h.setup_status = CV_ERR_SINGULAR;
+      return;
+    }
+  }
   if (!spd_inv_logdet_rt(h.L0, h.L0inv, &h.lnL0, d, h.wL, h.wJ, h.wM)) {
     h.setup_status = CV_ERR_NUMERIC;
     return;

@@ -74,6 +74,7 @@ struct PassKernel {
   int smem;  // dynamic shared memory bytes
   void (*tail)(const Hyp*, Ctl*, const double*, int, LsaLink);
   void (*batched)(BatchArgs);
+  void (*rate_inverse_test)(const double*, double*, double*, int*);
   void (*wishart_seg)(WishartArgs);
   void (*wishart_fin)(WishartArgs, const double*, const double*, double, uint64_t, double*, double*);
 };

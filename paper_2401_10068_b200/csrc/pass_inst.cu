@@ -20,6 +20,7 @@ static cavi::PassKernel make_kernel() {
   k.smem = G::kSmem;
   k.tail = cavi::tail_kernel<CAVI_D>;
   k.batched = cavi::batched_fit_kernel<CAVI_D>;
+  k.rate_inverse_test = cavi::rate_inverse_test_kernel<CAVI_D>;
   k.wishart_seg = cavi::wishart_segment_kernel<CAVI_D>;
   k.wishart_fin = cavi::wishart_finish_kernel<CAVI_D>;
   cudaFuncSetAttribute((const void*)k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem);

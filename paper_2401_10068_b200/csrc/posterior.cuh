@@ -163,7 +163,7 @@ __global__ void wishart_finish_kernel(WishartArgs a, const double* R, const doub
   // cov_k = inv(qv Lambda), Lk = chol(cov_k)  (Cholesky of the precision, then triangular inverse)
   double P[D * D], C[D * D], ld;
   for (int i = 0; i < D * D; ++i) P[i] = qv * L[i];
-  if (!spd_inv_logdet_t<D>(P, C, &ld)) {
+  if (!spd_inv_logdet_chol_t<D>(P, C, &ld)) {
     for (int i = 0; i < D; ++i) k_out[k * D + i] = qnan();
     return;
   }

@@ -14,9 +14,9 @@
 //            the previous state, the hyperparameters: ~110 words at d = 3, ~1.4k at d = 15) is
 //            gathered by all 32 lanes in one burst of independent loads -> one L2 round trip;
 //   phase 1  A^-1 G A^-1 and A^-1 g, element-parallel;
-//   phase 2  the new Q(Lambda) rate, one element per lane; its inverse + log-det with the
-//            jitter-once retry (linalg.py:279-298): Cholesky on lane 0 for d <= 4, the symmetric
-//            sweep across the warp above (tail_inverse);
+//   phase 2  the new Q(Lambda) rate, one element per lane; its inverse + log|det| with the
+//            reference's semantics (adjugate + det guard for d <= 3, pivoted elimination above,
+//            jitter-once retry, linalg.py:111-192, 279-298): lane 0 for d <= 3, the warp above;
 //   phase 3  the bound's three d x d contractions as lane partials + butterflies, the scalar
 //            assembly on lane 0; E[Lambda K] by rows; the deltas as warp max-reductions;
 //   phase 4  every store lane-parallel (state, trace entry, the next pass's generator).
@@ -36,7 +36,7 @@ struct TailSm {
   double k_old[D], l_old[D2], osc[4];     // previous state: k0k, lam0l_inv, (e_rho, a, b, ln|lam0l_inv|)
   double K0[D], L0[D2], L0i[D2];
   double hv[D], AG[D2], T[D2], k0c[D], dlt[D], k_new[D];
-  double L[D2], C[D2], S[D2], M[D2];
+  double L[D2], C[D2], S[D2], M[2 * D2];
   double ld;
   int ok;
 };
@@ -80,12 +80,12 @@ struct WarpLoad {
   }
 };
 
-// Inverse + log-det of the SPD rate in sm.C (modified by the jitter retry) -> sm.S; lane 0
-// holds *ld; returns ok (finite log-det) on every lane.  Up to kTailSerialD the whole
-// factorisation runs on lane 0 in registers (spd_inv_logdet_t: a d = 3 Cholesky + inverse is a
-// ~1k-cycle dependent chain); beyond it, the symmetric sweep across the warp
-// (spd_inv_logdet_sweep: d rounds of d^2/32 independent updates per lane).
-constexpr int kTailSerialD = 4;
+// Inverse + log|det| of the rate in sm.C -> sm.S, with the reference's semantics
+// (ref_inv_once_t: adjugate + |det| guard for d <= 3, pivoted elimination above; jitter-once
+// retry; no positive-definiteness test).  Lane 0 holds *ld; returns ok on every lane.  Up to
+// kTailSerialD on lane 0 in registers (a d = 3 adjugate is a short dependent chain); beyond
+// it, across the warp (ref_inv_logdet_warp).
+constexpr int kTailSerialD = 3;
 template <int D>
 __device__ __forceinline__ bool tail_inverse(TailSm<D>& sm, double* ld, int lane) {
   if constexpr (D <= kTailSerialD) {
@@ -104,7 +104,7 @@ __device__ __forceinline__ bool tail_inverse(TailSm<D>& sm, double* ld, int lane
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
   } else {
     double l = 0.0;
-    const bool ok = spd_inv_logdet_sweep<D>(sm.C, sm.S, &l, sm.M, lane);
+    const bool ok = ref_inv_logdet_warp<D>(sm.C, sm.AG, sm.M, sm.S, &l, lane);
     *ld = l;
     return __shfl_sync(0xffffffffu, (int)(ok && isfinite(l)), 0) != 0;
   }
@@ -585,6 +585,22 @@ __device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, co
     }
   }
   TAIL_PROF(*c, 5);
+}
+
+// Test hook (cv_test_rate_inverse): the tail's rate inversion on one given matrix, exactly as a
+// sweep runs it (tail_inverse: lane 0 for d <= kTailSerialD, the warp above).
+template <int D>
+__global__ void __launch_bounds__(32, 1) rate_inverse_test_kernel(const double* A, double* Ainv, double* ld, int* ok) {
+  __shared__ TailSm<D> sm;
+  for (int e = threadIdx.x; e < D * D; e += 32) sm.C[e] = A[e];
+  __syncwarp();
+  double l = 0.0;
+  const bool good = tail_inverse<D>(sm, &l, threadIdx.x);
+  for (int e = threadIdx.x; e < D * D; e += 32) Ainv[e] = sm.S[e];
+  if (threadIdx.x == 0) {
+    *ld = l;
+    *ok = good ? 1 : 0;
+  }
 }
 
 }  // namespace cavi

@@ -210,7 +210,7 @@ def vb_init(ds, hp) -> VbState:
     dds = device_dataset(ds)
     hs, keep = _lib.hyper_struct(hp)
     out = _lib.CvState()
-    _lib.check(_lib.lib().cv_init(dds.handle, C.byref(hs), C.byref(out)))
+    _lib.check(_lib.lib().cv_init(dds.handle, C.byref(hs), C.byref(out)), n_items=dds.V_total)
     return VbState(out, dds, hp)
 
 
@@ -255,7 +255,7 @@ def vb_fit(ds, hp, max_iter: int = 300, rel_tol: float = 1e-8, plan: linalg.Exec
     n = C.c_int32()
     _lib.check(_lib.lib().cv_fit(dds.handle, C.byref(hs), int(max_iter), float(rel_tol), int(bool(compute_elbo)),
                                  float(param_tol), C.byref(out), _lib.dptr(tr[0]), _lib.dptr(tr[1]),
-                                 _lib.dptr(tr[2]), _lib.dptr(tr[3]), C.byref(n)))
+                                 _lib.dptr(tr[2]), _lib.dptr(tr[3]), C.byref(n)), n_items=dds.V_total)
     k = n.value
     trace = VbTrace(elbo=tr[0, :k].copy(), delta_k0k=tr[1, :k].copy(), delta_rho=tr[2, :k].copy(),
                     delta_lam=tr[3, :k].copy())

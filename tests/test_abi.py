@@ -72,5 +72,5 @@ def test_status_codes_match_header():
     codes = {m.group(1): int(m.group(2)) for m in re.finditer(r"(CV_(?:OK|ERR_\w+))\s*=\s*(\d+)", text)}
     want = {"CV_OK": _lib.OK, "CV_ERR_NUMERIC": _lib.ERR_NUMERIC, "CV_ERR_NONFINITE": _lib.ERR_NONFINITE,
             "CV_ERR_ARG": _lib.ERR_ARG, "CV_ERR_CUDA": _lib.ERR_CUDA, "CV_ERR_IMPROPER": _lib.ERR_IMPROPER,
-            "CV_ERR_FORMAT": _lib.ERR_FORMAT, "CV_ERR_PEER": _lib.ERR_PEER}
+            "CV_ERR_FORMAT": _lib.ERR_FORMAT, "CV_ERR_PEER": _lib.ERR_PEER, "CV_ERR_SINGULAR": _lib.ERR_SINGULAR}
     assert codes == want
