@@ -440,9 +440,61 @@ __device__ bool ref_inv_once_warp(const double* A, double* M, double* Ainv, doub
   return true;
 }
 
-// ... with the jitter-once retry (linalg.py:279-298) on a jittered copy of A (A unchanged)
+// Symmetric sweep (Gauss-Jordan without pivoting: after sweeping every pivot k, W = -A^-1) --
+// the fast path for the positive-definite rates every real sweep produces: d rounds of d^2/32
+// branch-free updates per lane, no pivot search or row swaps.  Returns false on a non-positive
+// pivot (indefinite or singular), where the pivoted elimination decides as the reference would.
+template <int D>
+__device__ bool spd_sweep_warp(const double* A, double* W, double* Ainv, double* logabs, int lane) {
+  constexpr int D2 = D * D, K = (D2 + 31) / 32;
+  for (int e = lane; e < D2; e += 32) W[e] = A[e];
+  __syncwarp();
+  int ii[K], jj[K];
+#pragma unroll
+  for (int m = 0; m < K; ++m) {
+    const int e = lane + 32 * m < D2 ? lane + 32 * m : 0;
+    ii[m] = e / D;
+    jj[m] = e % D;
+  }
+  double prod = 1.0;
+  int ex = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const double p = W[k * D + k];
+    if (!(p > 0.0)) return false;  // every lane read the same pivot
+    const double rp = 1.0 / p;
+    double nv[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      const int i = ii[m], j = jj[m];
+      const double wik = W[i * D + k], wkj = W[k * D + j], we = W[i * D + j];
+      const double gen = fma(-wik * rp, wkj, we);
+      const double rowcol = (i == k ? wkj : wik) * rp;
+      nv[m] = (i == k && j == k) ? -rp : ((i == k || j == k) ? rowcol : gen);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < K; ++m)
+      if (lane + 32 * m < D2) W[lane + 32 * m] = nv[m];
+    __syncwarp();
+    if (lane == 0) {
+      prod *= p;
+      const int hi = __double2hiint(prod);
+      ex += ((hi >> 20) & 0x7ff) - 1023;
+      prod = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(prod));
+    }
+  }
+  for (int e = lane; e < D2; e += 32) Ainv[e] = -W[e];
+  if (lane == 0) *logabs = log(prod) + (double)ex * kLn2;
+  __syncwarp();
+  return true;
+}
+
+// The reference's inverse across the warp: the sweep when every pivot is positive, else the
+// pivoted elimination, with the jitter-once retry (linalg.py:279-298) on a jittered copy of A
 template <int D>
 __device__ bool ref_inv_logdet_warp(const double* A, double* J, double* M, double* Ainv, double* logdet, int lane) {
+  if (spd_sweep_warp<D>(A, M, Ainv, logdet, lane)) return true;
   if (ref_inv_once_warp<D>(A, M, Ainv, logdet, lane)) return true;
   double tr = 0.0;
   for (int j = 0; j < D; ++j) tr += A[j * D + j];  // every lane: the same sum
