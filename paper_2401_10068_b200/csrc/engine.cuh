@@ -705,24 +705,6 @@ __device__ __forceinline__ double elbo_t(const HypT<D>& h, double a, double b, c
   return t_lik + t_beta + t_k + t_lam + t_rho + h_beta + h_rho - e_lnq_k - e_lnq_lam;
 }
 
-// generator of the next pass from the current state (vb.py:136-144)
-template <int D>
-__device__ __forceinline__ void derive_pass_t(const HypT<D>& h, Ctl& c) {
-  cv_state& s = c.cur;
-  const double rnu = 1.0 / h.nu;
-#pragma unroll
-  for (int i = 0; i < D; ++i) c.pass.c[i] = s.k0k[i];
-#pragma unroll
-  for (int i = 0; i < D * D; ++i) {
-    c.pass.A[i] = s.e_lam[i];
-    c.pass.Ainv[i] = s.lam0l_inv[i] * rnu;
-  }
-  c.pass.lnA = D * h.ln_nu - s.ln_det_lam0l_inv;
-  c.pend_a = h.a_fit;
-  c.pend_b = h.b0 + 0.5 * s.resid;
-  c.pass.e_rho = c.pend_a / c.pend_b;
-}
-
 // runtime-d generator derivation (after a host-provided state)
 static __device__ __noinline__ void derive_pass_rt(const Hyp& h, Ctl& c) {
   const int d = h.d;
@@ -943,104 +925,6 @@ __device__ __forceinline__ void tail_t(const Hyp& hyp, Ctl& c, const double* sta
     c.pass.e_rho = h.a_fit / nb;
   }
   TAIL_PROF(c, 5);
-}
-
-// ------------------------------------------------------------------ EM (reference em.py)
-// One pass with the generator theta_n = (K, Lambda, Lambda^-1, rho) yields both
-//   the marginal log-likelihood of theta_n (model.py:278-287):
-//       ll = -1/2 [ V ln 2pi + sum ln den - V ln rho + sum rho (x - t)^2 / den ]   (= Ld, Q)
-//   and the E-step sums of em.py:44-77 for theta_{n+1} (g, G, R exactly as the VB pass).
-// The joint M-step (em.py:80-94), centred:  rho' = V / R,  h = Lambda^-1 g,  K' = K + h / V,
-//   Lambda'^-1 = Lambda^-1 + Lambda^-1 G Lambda^-1 / V - h h^T / V^2 ;  Lambda' = inv(.)
-// Loop bookkeeping of em_fit (em.py:97-124): trace entry n-1 is ll(theta_n); stop when
-// |ll_n - ll_{n-1}| < rel_tol |ll_n| or after max_iter M-steps.
-template <int D>
-__device__ __forceinline__ void em_tail_t(const Hyp& hyp, Ctl& c, const double* stats) {
-  HypT<D> h;
-  h.load(hyp);
-  GenT<D> gen;
-  gen.load(c.pass);
-  cv_state& s = c.cur;
-  const int n = c.iter;
-  const double V = h.V;
-  const double ll = -0.5 * (V * kLn2Pi + stats[stat_Ld(D)] - V * log(gen.e_rho) + stats[stat_Q(D)]);
-  int done = 0;
-  if (n >= 1) {
-    const int it = n - 1;
-    if (it < c.tr_cap) {
-      c.tr_elbo[it] = ll;
-      c.tr_drho[it] = gen.e_rho;
-      for (int j = 0; j < D; ++j) c.tr_k[(size_t)it * D + j] = gen.c[j];
-    }
-    if (fabs(ll - c.prev_elbo) < c.rel_tol * fabs(ll)) done = 1;
-    if (n >= c.max_iter) done = 1;
-  }
-  c.prev_elbo = ll;
-  s.d = D;
-  s.n_iter = n;
-  s.elbo = ll;
-  s.e_rho = gen.e_rho;
-  for (int j = 0; j < D; ++j) s.k0k[j] = gen.c[j];
-  for (int i = 0; i < D * D; ++i) {
-    s.lam0l_inv[i] = gen.A[i];  // EM: the current precision Lambda
-    s.e_lam[i] = gen.Ainv[i];   //     and its inverse
-  }
-  c.iter = n + 1;
-  if (done) {
-    c.done = 1;
-    return;
-  }
-  const double R = stats[stat_R(D)];
-  if (!(R > 0.0) || !isfinite(R)) {  // "non-positive residual sum in M-step" (em.py:85-86)
-    c.status = CV_ERR_NUMERIC;
-    c.done = 1;
-    return;
-  }
-  double G[D * D], hv[D], AG[D * D], Li[D * D], L[D * D], ld;
-  {
-    int p = D;
-    for (int j = 0; j < D; ++j)
-      for (int k = j; k < D; ++k) {
-        G[j * D + k] = stats[p];
-        G[k * D + j] = stats[p];
-        ++p;
-      }
-  }
-  const double* Ai = gen.Ainv;
-  for (int i = 0; i < D; ++i) {
-    double t = 0.0;
-    for (int j = 0; j < D; ++j) t += Ai[i * D + j] * stats[j];
-    hv[i] = t;
-  }
-  for (int i = 0; i < D; ++i)
-    for (int j = 0; j < D; ++j) {
-      double t = 0.0;
-      for (int k = 0; k < D; ++k) t += Ai[i * D + k] * G[k * D + j];
-      AG[i * D + j] = t;
-    }
-  const double rV = 1.0 / V;
-  for (int i = 0; i < D; ++i)
-    for (int j = i; j < D; ++j) {
-      double T = 0.0;
-      for (int k = 0; k < D; ++k) T += AG[i * D + k] * Ai[k * D + j];
-      const double v = 0.5 * (Ai[i * D + j] + Ai[j * D + i]) + T * rV - hv[i] * hv[j] * rV * rV;
-      Li[i * D + j] = v;
-      Li[j * D + i] = v;
-    }
-  if (!spd_inv_logdet_t<D>(Li, L, &ld)) {  // "M-step precision" inversion failed after jitter
-    c.status = CV_ERR_NUMERIC;
-    c.done = 1;
-    return;
-  }
-  for (int i = 0; i < D; ++i) {
-    c.pass.c[i] = gen.c[i] + hv[i] * rV;
-    for (int j = 0; j < D; ++j) {
-      c.pass.A[i * D + j] = 0.5 * (L[i * D + j] + L[j * D + i]);
-      c.pass.Ainv[i * D + j] = Li[i * D + j];
-    }
-  }
-  c.pass.lnA = -ld;
-  c.pass.e_rho = V / R;
 }
 
 }  // namespace cavi

@@ -297,33 +297,6 @@ __device__ __forceinline__ double gene_rows(const CK& k, double x, const double 
 // nobody waits for anybody.  Warp-level code: lane l handles statistics
 // l, l+32, ...
 
-// sum_{i<n} src[i*NS + stat] in the plan's fixed order: lane l adds rows l, l+32, l+64, ...
-// in index order, then a 32-lane xor butterfly (16, 8, 4, 2, 1); lane 0 writes.  One L2
-// round trip per 32 rows instead of a 16-deep dependent chain per stat column.
-template <int NS>
-__device__ __forceinline__ void warp_sum_rows(const double* src, int64_t n, double* dst, int lane) {
-  constexpr int B = NS < 16 ? NS : 16;  // stats per pass (register budget)
-  for (int s0 = 0; s0 < NS; s0 += B) {
-    double acc[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) acc[b] = 0.0;
-#pragma unroll 2
-    for (int64_t i = lane; i < n; i += 32) {
-      const double* row = src + i * NS + s0;
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (s0 + b < NS) acc[b] += __ldcg(row + b);
-    }
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      double v = acc[b];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0 && s0 + b < NS) dst[s0 + b] = v;
-    }
-  }
-}
-
 // lane 0 publishes (fence, cumulative over the warp's stores) and counts an arrival
 // (one acq_rel atomic: release publishes the warp's stores, which __syncwarp ordered before
 // lane 0's; acquire makes every other arriver's stores visible to the last one)
@@ -338,9 +311,10 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
-// The plan's fixed-order row sum (as warp_sum_rows: lane l adds rows l, l+32, ... from 0.0 in
-// index order, then the 16-8-4-2-1 xor butterfly) with the result left in registers: lane l
-// gets stat l + 32k in out[k].
+// The plan's fixed-order row sum -- lane l adds rows l, l+32, ... from 0.0 in index order, then
+// a 32-lane xor butterfly (16, 8, 4, 2, 1): one L2 round trip per 32 rows instead of a 16-deep
+// dependent chain per stat column -- with the result left in registers: lane l gets stat
+// l + 32k in out[k].
 template <int NS>
 __device__ __forceinline__ void warp_rows(const double* src, int64_t n, double (&out)[(NS + 31) / 32], int lane) {
   constexpr int B = NS < 16 ? NS : 16;
@@ -494,8 +468,7 @@ __device__ __forceinline__ bool warp_arrive_last_relaxed(unsigned int* counter, 
   return __shfl_sync(0xffffffffu, last, 0) != 0;
 }
 
-// The plan's fixed-order row sum (as warp_sum_rows: lane l adds rows l, l+32, ... from 0.0 in
-// index order, then the 16-8-4-2-1 xor butterfly) over n LL rows of NS values, polled until
+// The plan's fixed-order row sum (as warp_rows) over n LL rows of NS values, polled until
 // tagged `tag`; the result stays in registers: lane l gets stat l + 32k in out[k].
 template <int NS>
 __device__ __forceinline__ void warp_rows_ll(const uint64_t* rows, int64_t n, uint32_t tag,

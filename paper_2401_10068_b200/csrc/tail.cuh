@@ -4,7 +4,7 @@
 // reference's (K, Lambda) block (vb.py:172-197) in centred form, the rho block of the next
 // sweep (vb.py:141-144), the bound (vb.py:216-304), the fit loop's deltas and stop rule
 // (vb.py:307-347) and vb_init's globals (vb.py:82-111) -- the same per-element formulas as the
-// single-thread tail_t (engine.cuh), which the batched kernel keeps (one thread per fit).
+// single-thread tail_t (engine.cuh), which the batched kernel keeps (a fit group's first lane).
 //
 // Why a warp and shared memory: the tail is on the critical path of every sweep (the next
 // pass waits for it).  The single-thread version kept d x d blocks in registers / the stack
@@ -110,8 +110,13 @@ __device__ __forceinline__ bool tail_inverse(TailSm<D>& sm, double* ld, int lane
   }
 }
 
-// EM (reference em.py:44-124) from the same statistics, as em_tail_t (engine.cuh): the trace
-// entry of theta_n, the stop rule, then the joint M-step in centred form.  sm.hv / sm.T hold
+// EM (reference em.py:44-124) from the same statistics.  One pass with the generator
+// theta_n = (K, Lambda, Lambda^-1, rho) yields both the marginal log-likelihood of theta_n
+// (model.py:278-287: ll = -1/2 [V ln 2pi + sum ln den - V ln rho + sum rho (x - t)^2 / den] from
+// Ld and Q) and the E-step sums of em.py:44-77 for theta_{n+1}; the joint M-step (em.py:80-94)
+// in centred form: rho' = V / R, h = Lambda^-1 g, K' = K + h / V,
+// Lambda'^-1 = Lambda^-1 + Lambda^-1 G Lambda^-1 / V - h h^T / V^2, Lambda' = inv(.).  Trace entry
+// n-1 is ll(theta_n); stop when |ll_n - ll_{n-1}| < rel_tol |ll_n| or after max_iter M-steps.  sm.hv / sm.T hold
 // A^-1 g and A^-1 G A^-1 of the generator theta_n (phase 1 of tail_warp).
 template <int D>
 __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, double V, int n, int max_iter,
@@ -320,7 +325,7 @@ __device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, co
   __syncwarp();
   TAIL_PROF(*c, 6);
 
-  if (mode == MODE_EM) {  // em_tail_t (engine.cuh) across the warp
+  if (mode == MODE_EM) {  // EM's trace entry and M-step (em.py:80-124)
     em_tail_warp<D>(c, sm, lane, V, iter, max_iter, tr_cap, prev_elbo, rel_tol, g_erho, tr_elbo, tr_drho, tr_k);
     return;
   }
