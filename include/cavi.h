@@ -124,6 +124,14 @@ int32_t cv_dataset_generate(uint64_t seed, int64_t gene_lo, int64_t V, int64_t V
  * then contain commas and line breaks), with the same checks and messages. */
 int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, cv_dataset** out,
                             int32_t* n_networks);
+/* Binary dataset files (SURVEY 8(f) row 2's binary loader): the working arrays r (V,), mu (V,),
+ * D (V, d) as np.savez writes them (an uncompressed ZIP of '<f8' C-order .npy members, ZIP64
+ * for members over 4 GiB), streamed into HBM through pinned buffers and transformed on the
+ * device.  CV_ERR_FORMAT for anything else (compressed, other dtypes, missing members, shapes).
+ * cv_npz_probe validates the file on the host only (V, d). */
+int32_t cv_dataset_load_npz(const char* path, int32_t storage, int32_t device, cv_dataset** out,
+                            int32_t* n_networks);
+int32_t cv_npz_probe(const char* path, int64_t* V, int32_t* d);
 /* cli.write_dataset_csv (cli.py:47-56): header r,d_1..d_N, rows repr(r), untransformed profile
  * (D_j + mu, mu), every value formatted exactly as Python's repr(float).  threads <= 0: all cores. */
 int32_t cv_write_dataset_csv(const char* path, const double* r, const double* mu, const double* D, int64_t V,

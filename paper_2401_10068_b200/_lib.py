@@ -94,6 +94,8 @@ _SIGS = {
     "cv_em_fit": (C.c_int32, [C.c_void_p, _D, _D, C.c_double, C.c_int32, C.c_double, _D, _D, _D, _D, _D, _D,
                               _P(C.c_int32)]),
     "cv_dataset_load_csv": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, _P(C.c_void_p), _P(C.c_int32)]),
+    "cv_dataset_load_npz": (C.c_int32, [C.c_char_p, C.c_int32, C.c_int32, _P(C.c_void_p), _P(C.c_int32)]),
+    "cv_npz_probe": (C.c_int32, [C.c_char_p, _P(C.c_int64), _P(C.c_int32)]),
     "cv_write_dataset_csv": (C.c_int32, [C.c_char_p, _D, _D, _D, C.c_int64, C.c_int32, C.c_int32]),
     "cv_parse_number_host": (C.c_int32, [C.c_char_p, C.c_int64, _D]),
     "cv_format_repr": (C.c_int32, [C.c_double, C.c_char_p]),

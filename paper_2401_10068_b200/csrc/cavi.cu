@@ -592,6 +592,9 @@ int run_groups(cv_dataset* ds, int need) {
 }
 
 template <typename T>
+int transform_staged(cv_dataset* ds, double* dr, double* dmu, double* dD);
+
+template <typename T>
 int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, const double* D) {
   // stage the host arrays in HBM, then transform into the SoA stream
   double *dr = nullptr, *dmu = nullptr, *dD = nullptr;
@@ -602,6 +605,12 @@ int create_storage_kernels(cv_dataset* ds, const double* r, const double* mu, co
   CK(cudaMemcpyAsync(dr, r, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
   CK(cudaMemcpyAsync(dmu, mu, sizeof(double) * V, cudaMemcpyHostToDevice, ds->stream));
   CK(cudaMemcpyAsync(dD, D, sizeof(double) * V * ds->d, cudaMemcpyHostToDevice, ds->stream));
+  return transform_staged<T>(ds, dr, dmu, dD);
+}
+
+// r, mu, D (row-major) already in HBM (pool allocations): the SoA stream; r and mu are kept
+template <typename T>
+int transform_staged(cv_dataset* ds, double* dr, double* dmu, double* dD) {
   const int tb = 256;
   const int64_t blocks = (ds->Vp + tb - 1) / tb;
   if (blocks > 0) {
@@ -1422,6 +1431,210 @@ int32_t cv_dataset_load_csv(const char* path, int32_t storage, int32_t device, c
   if (n_networks) *n_networks = N;
   return CV_OK;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- binary dataset files (.npz)
+// The Dataset's working arrays r (V,), mu (V,), D (V, d) as np.savez writes them: a ZIP of
+// STORED (uncompressed) .npy members, ZIP64 extra fields for members over 4 GiB.  The host
+// walks the local file headers and the .npy headers (format 1.0-3.0, '<f8', C order) and streams
+// the raw bytes into HBM through pinned buffers; the stream layout is built on the device.
+namespace {
+
+struct NpyMember {
+  std::string name;
+  int64_t data_off = 0, nbytes = 0;
+  std::vector<int64_t> shape;
+};
+
+uint32_t rd32(const unsigned char* p) { return p[0] | (p[1] << 8) | (p[2] << 16) | ((uint32_t)p[3] << 24); }
+uint16_t rd16(const unsigned char* p) { return (uint16_t)(p[0] | (p[1] << 8)); }
+uint64_t rd64(const unsigned char* p) { return (uint64_t)rd32(p) | ((uint64_t)rd32(p + 4) << 32); }
+
+int npz_bad(const char* path, const char* why) {
+  return fail(CV_ERR_FORMAT, "%s: not a dataset .npz (np.savez of r, mu, D as float64): %s", path, why);
+}
+
+// the .npy header of a member: '<f8', C order, its shape; data_off moves past the header
+int npy_header(int fd, const char* path, NpyMember* m) {
+  unsigned char pre[12];
+  if (pread(fd, pre, sizeof pre, m->data_off) != (ssize_t)sizeof pre) return npz_bad(path, "short .npy header");
+  if (std::memcmp(pre, "\x93NUMPY", 6) != 0) return npz_bad(path, "member is not a .npy array");
+  const int major = pre[6];
+  const int64_t hlen = major == 1 ? rd16(pre + 8) : rd32(pre + 8);
+  const int64_t hoff = major == 1 ? 10 : 12;
+  if (hlen <= 0 || hlen > (1 << 20)) return npz_bad(path, "bad .npy header length");
+  std::string h((size_t)hlen, '\0');
+  if (pread(fd, &h[0], (size_t)hlen, m->data_off + hoff) != (ssize_t)hlen) return npz_bad(path, "short .npy header");
+  auto field = [&](const char* key) -> std::string {
+    const size_t k = h.find(key);
+    if (k == std::string::npos) return "";
+    size_t a = h.find(':', k);
+    return a == std::string::npos ? "" : h.substr(a + 1);
+  };
+  const std::string descr = field("'descr'"), fo = field("'fortran_order'"), shp = field("'shape'");
+  if (descr.find("'<f8'") == std::string::npos && descr.find("'f8'") == std::string::npos)
+    return npz_bad(path, ("member " + m->name + " is not float64").c_str());
+  if (fo.find("False") == std::string::npos || fo.find("False") > fo.find(','))
+    return npz_bad(path, ("member " + m->name + " is not C-ordered").c_str());
+  const size_t a = shp.find('('), b = shp.find(')');
+  if (a == std::string::npos || b == std::string::npos || b < a) return npz_bad(path, "bad .npy shape");
+  m->shape.clear();
+  for (size_t i = a + 1; i < b;) {
+    while (i < b && (shp[i] == ' ' || shp[i] == ',')) ++i;
+    if (i >= b) break;
+    char* end = nullptr;
+    const long long v = std::strtoll(shp.c_str() + i, &end, 10);
+    if (end == shp.c_str() + i || v < 0) return npz_bad(path, "bad .npy shape");
+    m->shape.push_back(v);
+    i = (size_t)(end - shp.c_str());
+  }
+  int64_t n = 1;
+  for (int64_t v : m->shape) n *= v;
+  m->data_off += hoff + hlen;
+  if (m->nbytes - hoff - hlen != n * 8) return npz_bad(path, "member size does not match its shape");
+  m->nbytes = n * 8;
+  return CV_OK;
+}
+
+int npz_members(int fd, int64_t size, const char* path, std::vector<NpyMember>* out) {
+  int64_t off = 0;
+  unsigned char hd[30];
+  while (off + 30 <= size && pread(fd, hd, 30, off) == 30 && rd32(hd) == 0x04034b50u) {
+    const uint16_t flags = rd16(hd + 6), method = rd16(hd + 8), nlen = rd16(hd + 26), xlen = rd16(hd + 28);
+    uint64_t csize = rd32(hd + 18), usize = rd32(hd + 22);
+    if (method != 0) return npz_bad(path, "compressed member (np.savez_compressed): use np.savez");
+    if (flags & 8) return npz_bad(path, "streamed ZIP members (data descriptors) are not supported");
+    std::vector<unsigned char> nx((size_t)nlen + xlen);
+    if (pread(fd, nx.data(), nx.size(), off + 30) != (ssize_t)nx.size()) return npz_bad(path, "short ZIP header");
+    for (size_t x = nlen; x + 4 <= nx.size();) {  // ZIP64 extended information
+      const uint16_t id = rd16(&nx[x]), len = rd16(&nx[x + 2]);
+      if (id == 0x0001) {
+        size_t q = x + 4;
+        if (usize == 0xffffffffu && q + 8 <= x + 4 + len) {
+          usize = rd64(&nx[q]);
+          q += 8;
+        }
+        if (csize == 0xffffffffu && q + 8 <= x + 4 + len) csize = rd64(&nx[q]);
+      }
+      x += 4 + len;
+    }
+    NpyMember m;
+    m.name.assign((const char*)nx.data(), nlen);
+    m.data_off = off + 30 + nlen + xlen;
+    m.nbytes = (int64_t)csize;
+    if (csize != usize || m.data_off + m.nbytes > size) return npz_bad(path, "inconsistent ZIP member sizes");
+    out->push_back(m);
+    off = m.data_off + m.nbytes;
+  }
+  if (out->empty()) return npz_bad(path, "no ZIP members");
+  return CV_OK;
+}
+
+// r, mu, D members with consistent shapes -> V, d
+int npz_dataset(int fd, int64_t size, const char* path, NpyMember* r, NpyMember* mu, NpyMember* D) {
+  std::vector<NpyMember> ms;
+  int rc = npz_members(fd, size, path, &ms);
+  if (rc) return rc;
+  NpyMember* want[3] = {r, mu, D};
+  const char* names[3] = {"r.npy", "mu.npy", "D.npy"};
+  for (int k = 0; k < 3; ++k) {
+    bool found = false;
+    for (auto& m : ms)
+      if (m.name == names[k]) {
+        *want[k] = m;
+        found = true;
+      }
+    if (!found) return npz_bad(path, (std::string("missing member ") + names[k]).c_str());
+    if ((rc = npy_header(fd, path, want[k]))) return rc;
+  }
+  if (r->shape.size() != 1 || mu->shape != r->shape || D->shape.size() != 2 || D->shape[0] != r->shape[0] ||
+      D->shape[1] < 1)
+    return npz_bad(path, "shapes must be r (V,), mu (V,), D (V, d)");
+  if (r->shape[0] < 1) return fail(CV_ERR_ARG, "no records");
+  return CV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cv_npz_probe(const char* path, int64_t* V, int32_t* d) {
+  if (!path || !V || !d) return fail(CV_ERR_ARG, "null pointer");
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  struct stat sb;
+  int rc = fstat(fd, &sb) == 0 ? CV_OK : fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  NpyMember r, mu, D;
+  if (rc == CV_OK) rc = npz_dataset(fd, (int64_t)sb.st_size, path, &r, &mu, &D);
+  close(fd);
+  if (rc) return rc;
+  *V = r.shape[0];
+  *d = (int32_t)D.shape[1];
+  return CV_OK;
+}
+
+int32_t cv_dataset_load_npz(const char* path, int32_t storage, int32_t device, cv_dataset** out,
+                            int32_t* n_networks) {
+  if (!path || !out) return fail(CV_ERR_ARG, "null pointer");
+  LoadScratch sc;
+  sc.fd = open(path, O_RDONLY);
+  if (sc.fd < 0) return fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  struct stat sb;
+  if (fstat(sc.fd, &sb) != 0) return fail(CV_ERR_ARG, "%s: %s", path, strerror(errno));
+  NpyMember mr, mmu, mD;
+  int rc = npz_dataset(sc.fd, (int64_t)sb.st_size, path, &mr, &mmu, &mD);
+  if (rc) return rc;
+  const int64_t V = mr.shape[0];
+  const int d = (int)mD.shape[1];
+  if (d > kMaxD) return fail(CV_ERR_ARG, "dimension %d unsupported (1..%d)", d, kMaxD);
+  cv_dataset* ds = nullptr;
+  if ((rc = new_dataset(V, d, 0, V, storage, device, &ds))) return rc;
+  auto bail = [&](int code) {
+    std::string keep = g_err;
+    cv_dataset_destroy(ds);
+    g_err = keep;
+    return code;
+  };
+  double *dr = nullptr, *dmu = nullptr, *dD = nullptr;
+  if (pool_alloc((void**)&dr, sizeof(double) * V, ds->stream, device) != cudaSuccess ||
+      pool_alloc((void**)&dmu, sizeof(double) * V, ds->stream, device) != cudaSuccess ||
+      pool_alloc((void**)&dD, sizeof(double) * V * d, ds->stream, device) != cudaSuccess)
+    return bail(fail(CV_ERR_CUDA, "cudaMallocAsync"));
+  // file -> HBM through two pinned staging buffers (the reads overlap the copies)
+  const size_t kStage = (size_t)64 << 20;
+  for (int b = 0; b < 2; ++b)
+    if (cudaHostAlloc(&sc.pinned[b], kStage, cudaHostAllocDefault) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sc.ev[b], cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(CV_ERR_CUDA, "pinned staging"));
+  const NpyMember* mem[3] = {&mr, &mmu, &mD};
+  char* dst[3] = {(char*)dr, (char*)dmu, (char*)dD};
+  int64_t k = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int64_t pos = 0; pos < mem[a]->nbytes; ++k) {
+      const int b = (int)(k & 1);
+      if (k >= 2 && cudaEventSynchronize(sc.ev[b]) != cudaSuccess) return bail(fail(CV_ERR_CUDA, "staging"));
+      const size_t n = (size_t)std::min<int64_t>((int64_t)kStage, mem[a]->nbytes - pos);
+      for (size_t got = 0; got < n;) {
+        const ssize_t m = pread(sc.fd, (char*)sc.pinned[b] + got, n - got, mem[a]->data_off + pos + (int64_t)got);
+        if (m <= 0) return bail(fail(CV_ERR_ARG, "%s: short read", path));
+        got += (size_t)m;
+      }
+      if (cudaMemcpyAsync(dst[a] + pos, sc.pinned[b], n, cudaMemcpyHostToDevice, ds->stream) != cudaSuccess ||
+          cudaEventRecord(sc.ev[b], ds->stream) != cudaSuccess)
+        return bail(fail(CV_ERR_CUDA, "cudaMemcpyAsync"));
+      pos += (int64_t)n;
+    }
+  rc = f32_stream(storage) ? transform_staged<float>(ds, dr, dmu, dD) : transform_staged<double>(ds, dr, dmu, dD);
+  if (rc) return bail(rc);
+  *out = ds;
+  if (n_networks) *n_networks = d + 1;
+  return CV_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
 
 int32_t cv_dataset_info(cv_dataset* ds, int64_t* V, int32_t* d, int64_t* gene_lo, int64_t* V_total, int32_t* storage,
                         int64_t* device_bytes) {

@@ -22,7 +22,8 @@ import numpy as np
 from . import _lib, model
 from ._lib import UsageError
 
-__all__ = ["UsageError", "load_dataset_csv", "read_dataset_csv", "write_dataset_csv"]
+__all__ = ["UsageError", "load_dataset_csv", "load_dataset_npz", "read_dataset_csv", "read_dataset_npz",
+           "write_dataset_csv", "write_dataset_npz"]
 
 
 def _open_check(path) -> bytes:
@@ -67,3 +68,43 @@ def write_dataset_csv(path, ds, threads: int = 0) -> None:
     V, d = D.shape
     _lib.check(_lib.lib().cv_write_dataset_csv(os.fspath(path).encode(), _lib.dptr(r), _lib.dptr(mu), _lib.dptr(D),
                                                V, d, int(threads)))
+
+
+# ---------------------------------------------------------------- binary (.npz) dataset files
+def write_dataset_npz(path, ds) -> None:
+    """The Dataset's working arrays r (V,), mu (V,), D (V, d) as an uncompressed np.savez file
+    (any numpy reads it back with np.load); the fast path for datasets too large for CSV."""
+    if isinstance(ds, model.DeviceDataset):
+        r, mu, D = ds.download()
+    else:
+        r, mu, D = (np.ascontiguousarray(a, dtype=np.float64) for a in (ds.r, ds.mu, np.atleast_2d(ds.D)))
+    with open(os.fspath(path), "wb") as fh:  # an open file: np.savez does not append ".npz"
+        np.savez(fh, r=r, mu=mu, D=D)
+
+
+def npz_info(path):
+    """(V, d) of a dataset .npz, validated on the host (no GPU needed)."""
+    p = _open_check(path)
+    V, d = C.c_int64(), C.c_int32()
+    _lib.check(_lib.lib().cv_npz_probe(p, C.byref(V), C.byref(d)))
+    return V.value, d.value
+
+
+def load_dataset_npz(path, storage: str = "f64", device: int | None = None) -> model.DeviceDataset:
+    """A dataset .npz (write_dataset_npz / np.savez of r, mu, D) streamed into HBM."""
+    p = _open_check(path)
+    h, n = C.c_void_p(), C.c_int32()
+    _lib.check(_lib.lib().cv_dataset_load_npz(p, model._STORAGE[storage],
+                                              _lib.default_device() if device is None else device,
+                                              C.byref(h), C.byref(n)))
+    return model.DeviceDataset(h.value, n.value)
+
+
+def read_dataset_npz(path) -> model.Dataset:
+    """The host Dataset of a dataset .npz, its HBM stream attached (as read_dataset_csv)."""
+    from . import vb  # noqa: PLC0415
+
+    dd = load_dataset_npz(path)
+    ds = dd.to_host()
+    vb.keep_resident(ds, dd)
+    return ds

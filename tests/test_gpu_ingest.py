@@ -128,3 +128,37 @@ def test_read_dataset_keeps_its_hbm_stream(ing):
     assert vb.device_dataset(ds) is dd and dd.V == ds.V
     x = dd.stream_x()
     assert np.array_equal(bits(x), bits(ds.r - ds.mu))
+
+
+@pytest.mark.parametrize("storage", ["f64", "f32", "f32m"])
+def test_npz_round_trip_into_hbm(ing, tmp_path, storage):
+    """Binary dataset files: write_dataset_npz -> load_dataset_npz reproduces the stream the
+    upload path builds, bit for bit, and a fit on it equals the fit on the uploaded dataset."""
+    from paper_2401_10068_b200 import model, vb
+
+    src = model.regime(300_001, 17, 4)
+    r, mu, D = src.download()
+    ds = model.Dataset(r=r, mu=mu, D=D, n_networks=4)
+    p = tmp_path / "ds.npz"
+    ing.write_dataset_npz(p, ds)
+    dd = ing.load_dataset_npz(p, storage=storage)
+    assert dd.V == 300_001 and dd.dim == 3 and dd.n_networks == 4 and dd.storage == storage
+    up = model.upload(ds, storage=storage)
+    assert np.array_equal(bits(dd.stream_x()), bits(up.stream_x()))
+    r2, mu2, D2 = dd.download()
+    assert np.array_equal(bits(r2), bits(r)) and np.array_equal(bits(mu2), bits(mu)) and np.array_equal(bits(D2), bits(D))
+    hp = model.default_hyperparams(4)
+    s1, t1 = vb.vb_fit(dd, hp, max_iter=12)
+    s2, t2 = vb.vb_fit(up, hp, max_iter=12)
+    assert np.array_equal(t1.elbo, t2.elbo) and np.array_equal(s1.k0k, s2.k0k)
+
+
+def test_read_dataset_npz_keeps_its_hbm_stream(ing, tmp_path):
+    from paper_2401_10068_b200 import model, vb
+
+    r, mu, D = model.regime(5000, 3, 3).download()
+    p = tmp_path / "ds.npz"
+    ing.write_dataset_npz(p, model.Dataset(r=r, mu=mu, D=D, n_networks=3))
+    ds = ing.read_dataset_npz(p)
+    assert np.array_equal(bits(ds.r), bits(r)) and np.array_equal(bits(ds.D), bits(D)) and ds.n_networks == 3
+    assert vb.device_dataset(ds).V == 5000

@@ -84,3 +84,28 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def bench_npz(V=100_000_000, N=4):
+    """Binary dataset file -> HBM (load_dataset_npz) at V genes."""
+    import tempfile
+
+    from paper_2401_10068_b200 import ingest, model
+
+    dd = model.regime(V, 2026, N)
+    with tempfile.TemporaryDirectory() as tmp:
+        p = os.path.join(tmp, "ds.npz")
+        t = time.time()
+        ingest.write_dataset_npz(p, dd)
+        tw = time.time() - t
+        size = os.path.getsize(p)
+        loads = []
+        for _ in range(3):
+            t = time.time()
+            d2 = ingest.load_dataset_npz(p)
+            loads.append(time.time() - t)
+            same = np.array_equal(d2.stream_x(), dd.stream_x())
+            d2.close()
+    print(json.dumps({"what": "dataset .npz -> HBM dataset (ingest.load_dataset_npz)", "rows": V, "N": N,
+                      "file_bytes": size, "write_s": tw, "load_s_best": min(loads), "load_s_all": loads,
+                      "file_GB_per_s": size / min(loads) / 1e9, "stream_bit_exact": bool(same)}), flush=True)
