@@ -117,6 +117,7 @@ struct cv_dataset {
   unsigned long long* ticket = nullptr;
   uint64_t* opartials = nullptr;     // [8][ns][2] LL words
   int n_live_octants = 0;
+  int oct_last = 0;
   int* flags = nullptr;              // [0] bad input bits, [1] scratch status
   Ctl* ctl = nullptr;
   Hyp* hyp = nullptr;
@@ -184,14 +185,18 @@ struct CallScratch {
   }
 };
 
-// octants of this shard that hold groups
+// octants of this shard that hold groups, and the last of them
 void count_live_octants(cv_dataset* ds) {
   ds->n_live_octants = 0;
+  ds->oct_last = ds->oct_lo;
   for (int q = ds->oct_lo; q < ds->oct_hi; ++q) {
     const int64_t h0 = std::max<int64_t>((int64_t)q * ds->groups_per_octant, ds->group_lo);
     const int64_t h1 = std::min<int64_t>(std::min<int64_t>((int64_t)(q + 1) * ds->groups_per_octant, ds->n_groups_total),
                                          ds->group_lo + ds->n_groups);
-    if (h1 > h0) ++ds->n_live_octants;
+    if (h1 > h0) {
+      ++ds->n_live_octants;
+      ds->oct_last = q;
+    }
   }
 }
 
@@ -292,6 +297,7 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.odone = ds->counters + ds->n_groups + kOctants;
   a.pass_seq = ds->counters + ds->n_groups + kOctants + 1;
   a.opartials = ds->opartials;
+  a.oct_last = ds->oct_last;
   a.ticket = ds->ticket;
   a.n_live_octants = ds->n_live_octants;
   a.ctl = ds->ctl;

@@ -52,8 +52,9 @@ struct PassArgs {
   uint64_t* gpartials;     // [n_groups][ns][2] group sums, LL
   unsigned int* gcount;    // [n_groups] arrivals per group
   unsigned int* ocount;    // [8] arrivals per octant
-  unsigned int* odone;     // [1] completed octants
+  unsigned int* odone;     // [1] completed octants (acquire/release cascade)
   uint64_t* opartials;     // [8][ns][2] octant sums, LL
+  int oct_last;            // the shard's last octant holding groups (the LL cascade's final level)
   unsigned int* pass_seq;  // [1] passes completed on this dataset = the LL tag of the running pass
   unsigned long long* ticket;  // chunk tickets (monotone across sweeps)
   int n_live_octants;      // octants of this shard holding at least one group
@@ -552,11 +553,15 @@ __device__ __forceinline__ void finish_chunk_ll(const PassArgs& a, int64_t chunk
     if (lane == 0) a.ocount[o] = 0u;
     warp_rows_ll<NS>(a.gpartials + (g0 - a.group_lo) * NS * 2, g1 - g0, tag, osum, lane);
   }
-  ll_put_row<NS>(a.opartials + o * NS * 2, osum, tag, lane);
-  if (!warp_arrive_last_relaxed(a.odone, (unsigned int)a.n_live_octants, lane)) return;
-  // every octant this shard owns is complete: pairwise tree over them (empty octants add 0);
-  // this warp's own octant from registers, the others' loads all in flight together
-  if (lane == 0) *a.odone = 0u;
+  // No arrival level for the shard total: the warp that completes the shard's LAST octant
+  // builds it, polling the other octants' rows.  It can only wait on octants whose chunks sit
+  // in other CTAs' pipelines (it completed the last octant, so this CTA's chunks -- dispatched in
+  // increasing order -- are all done): no chain of waits; in practice the lower octants were
+  // complete long before and the poll is one round trip.
+  if (o != a.oct_last) {
+    ll_put_row<NS>(a.opartials + o * NS * 2, osum, tag, lane);
+    return;
+  }
   if (a.cta_trace && lane == 0) {
     a.cta_trace[blockIdx.x * 8 + 4] = t_entry;
     a.cta_trace[blockIdx.x * 8 + 5] = globaltimer_ns();
