@@ -441,42 +441,49 @@ __device__ bool ref_inv_once_warp(const double* A, double* M, double* Ainv, doub
 }
 
 // Symmetric sweep (Gauss-Jordan without pivoting: after sweeping every pivot k, W = -A^-1) --
-// the fast path for the positive-definite rates every real sweep produces: d rounds of d^2/32
-// branch-free updates per lane, no pivot search or row swaps.  Returns false on a non-positive
-// pivot (indefinite or singular), where the pivoted elimination decides as the reference would.
+// the fast path for the positive-definite rates every real sweep produces.  W lives in
+// registers: lane r + 16 h holds row r's column half h (H = ceil(d / 2) columns), so a pivot is
+// 2 + H shuffles (pivot, column k, row k) and H branch-free updates per lane, with no shared-memory
+// round trip or warp barrier between pivots (one warp alone runs the tail: every pivot is pure
+// latency).  Returns false on a non-positive pivot (indefinite or singular), where the pivoted
+// elimination decides as the reference would.
 template <int D>
-__device__ bool spd_sweep_warp(const double* A, double* W, double* Ainv, double* logabs, int lane) {
-  constexpr int D2 = D * D, K = (D2 + 31) / 32;
-  for (int e = lane; e < D2; e += 32) W[e] = A[e];
-  __syncwarp();
-  int ii[K], jj[K];
+__device__ bool spd_sweep_warp(const double* A, double* /*W*/, double* Ainv, double* logabs, int lane) {
+  static_assert(D <= 16, "two column halves of at most 16 rows");
+  constexpr int H = (D + 1) / 2;
+  const int r = lane & 15, h = lane >> 4;
+  double w[H];
 #pragma unroll
-  for (int m = 0; m < K; ++m) {
-    const int e = lane + 32 * m < D2 ? lane + 32 * m : 0;
-    ii[m] = e / D;
-    jj[m] = e % D;
+  for (int t = 0; t < H; ++t) {
+    const int j = h * H + t;
+    w[t] = (r < D && j < D) ? A[r * D + j] : 0.0;
   }
   double prod = 1.0;
   int ex = 0;
+  // Rolled over the column half of the pivot, unrolled within it (the register index of the
+  // pivot's column must be static: a dynamic index goes to local memory).  The tail runs once
+  // per sweep with its code fetched cold; the half-rolled form measured fastest in the tail at
+  // d = 15 (tools/tail_cycles.sh: unrolled 9.3k, half-rolled 7.7k, fully rolled with selects 8.4k cycles).
+#pragma unroll 1
+  for (int hk = 0; hk < 2; ++hk)
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const double p = W[k * D + k];
-    if (!(p > 0.0)) return false;  // every lane read the same pivot
+  for (int tk = 0; tk < H; ++tk) {
+    const int k = hk * H + tk;
+    if (k >= D) break;
+    const double p = __shfl_sync(0xffffffffu, w[tk], k + 16 * hk);
+    const double wik = __shfl_sync(0xffffffffu, w[tk], r + 16 * hk);
+    double wkj[H];
+#pragma unroll
+    for (int t = 0; t < H; ++t) wkj[t] = __shfl_sync(0xffffffffu, w[t], k + 16 * h);
+    if (!(p > 0.0)) return false;  // every lane has the same pivot
     const double rp = 1.0 / p;
-    double nv[K];
 #pragma unroll
-    for (int m = 0; m < K; ++m) {
-      const int i = ii[m], j = jj[m];
-      const double wik = W[i * D + k], wkj = W[k * D + j], we = W[i * D + j];
-      const double gen = fma(-wik * rp, wkj, we);
-      const double rowcol = (i == k ? wkj : wik) * rp;
-      nv[m] = (i == k && j == k) ? -rp : ((i == k || j == k) ? rowcol : gen);
+    for (int t = 0; t < H; ++t) {
+      const int j = h * H + t;
+      const double gen = fma(-wik * rp, wkj[t], w[t]);
+      const double rowcol = (r == k ? wkj[t] : wik) * rp;
+      w[t] = (r == k && j == k) ? -rp : ((r == k || j == k) ? rowcol : gen);
     }
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < K; ++m)
-      if (lane + 32 * m < D2) W[lane + 32 * m] = nv[m];
-    __syncwarp();
     if (lane == 0) {
       prod *= p;
       const int hi = __double2hiint(prod);
@@ -484,7 +491,11 @@ __device__ bool spd_sweep_warp(const double* A, double* W, double* Ainv, double*
       prod = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, __double2loint(prod));
     }
   }
-  for (int e = lane; e < D2; e += 32) Ainv[e] = -W[e];
+#pragma unroll
+  for (int t = 0; t < H; ++t) {
+    const int j = h * H + t;
+    if (r < D && j < D) Ainv[r * D + j] = -w[t];
+  }
   if (lane == 0) *logabs = log(prod) + (double)ex * kLn2;
   __syncwarp();
   return true;

@@ -41,8 +41,12 @@ struct TailSm {
   int ok;
 };
 
+// Warp reductions.  Each starts with __syncwarp(): the lane-strided loops before them (an
+// unrolled `if (e >= D2) break`) leave the warp diverged, and a shuffle in a diverged warp
+// takes the emulated collective path (WARPSYNC.COLLECTIVE, ~10x the instructions).
 // NaN-propagating max over the warp (rel_delta_t's `df > md || df != df`)
 __device__ __forceinline__ double warp_max_nan(double v) {
+  __syncwarp();
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const double o = __shfl_xor_sync(0xffffffffu, v, off);
@@ -51,11 +55,13 @@ __device__ __forceinline__ double warp_max_nan(double v) {
   return v;
 }
 __device__ __forceinline__ double warp_fmax(double v) {
+  __syncwarp();
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
   return v;
 }
 __device__ __forceinline__ double warp_sum(double v) {
+  __syncwarp();
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
@@ -160,6 +166,7 @@ __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, do
     s.lam0l_inv[e] = sm.gA[e];  // EM: the current precision Lambda
     s.e_lam[e] = sm.gAi[e];     //     and its inverse
   }
+  __syncwarp();
   if (__shfl_sync(0xffffffffu, done, 0)) return;
   const double rV = 1.0 / V;
   #pragma unroll
@@ -399,6 +406,7 @@ __device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, co
   double elbo = qnan();
   int elbo_status = CV_OK;
   if (status == CV_OK && (compute_elbo || mode != MODE_SWEEP) && lane == 0 && !proper_q) elbo_status = CV_ERR_IMPROPER;
+  __syncwarp();
   elbo_status = __shfl_sync(0xffffffffu, elbo_status, 0);
   const bool want_elbo = __shfl_sync(0xffffffffu, (int)(status == CV_OK && (compute_elbo || mode != MODE_SWEEP)), 0);
   if (want_elbo && elbo_status == CV_OK) {
