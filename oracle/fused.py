@@ -24,8 +24,10 @@ Algebra (reference vb.py:129-198 and vb.py:216-304 rewritten):
   O(d^3) with centred (cancellation-free) formulas.
 
 Reduction plan (GPU-count invariant, deterministic):
-  chunk  = CHUNK_GENES consecutive genes  -> one partial
-  group  = GROUP_CHUNKS consecutive chunks, summed by warp_rows_sum (strided lanes + butterfly)
+  chunk  = plan_chunk_genes(V, d) consecutive genes (4096, or 8192 for d >= 3 and
+           V >= 2^23: engine.cuh plan_chunk_genes)  -> one partial
+  group  = GROUP_GENES (262144) consecutive genes = its chunks, summed by warp_rows_sum
+           (strided lanes + butterfly)
   octant = ceil(n_groups/8) consecutive groups, summed by warp_rows_sum
   total  = pairwise tree over the 8 octants ((o0+o1)+(o2+o3))+((o4+o5)+(o6+o7))
 A rank of a power-of-two world G<=8 owns 8/G consecutive octants, reduces
@@ -42,8 +44,14 @@ from scipy.special import digamma, gammaln, multigammaln
 
 from .cavi import Hyper, NumericFailure
 
-CHUNK_GENES = 4096
-GROUP_CHUNKS = 64
+CHUNK_GENES = 4096  # the smallest chunk
+GROUP_CHUNKS = 64   # chunks of CHUNK_GENES per group
+GROUP_GENES = CHUNK_GENES * GROUP_CHUNKS
+
+
+def plan_chunk_genes(V_total: int, d: int) -> int:
+    """Genes per chunk of a dataset (engine.cuh plan_chunk_genes)."""
+    return 8192 if d >= 3 and V_total >= (1 << 23) else CHUNK_GENES
 N_OCTANTS = 8
 LN2PI = np.log(2.0 * np.pi)
 
@@ -66,7 +74,7 @@ class Plan:
     groups_per_octant: int
 
     def octant_genes(self, o: int):
-        per = self.groups_per_octant * GROUP_CHUNKS * CHUNK_GENES
+        per = self.groups_per_octant * GROUP_GENES
         lo = min(o * per, self.V)
         return lo, min(lo + per, self.V)
 
@@ -124,6 +132,7 @@ def local_stats(x, D, gen: Generator, gene_lo: int, V_total: int):
     """Per-octant sums of genes [gene_lo, gene_lo+len(x)) (zeros outside the range)."""
     p = make_plan(V_total)
     ns = n_stats(D.shape[1])
+    cg = plan_chunk_genes(V_total, D.shape[1])
     terms = gene_terms(x, D, gen) if x.shape[0] else np.zeros((0, ns))
     octs = []
     for o in range(N_OCTANTS):
@@ -134,9 +143,9 @@ def local_stats(x, D, gen: Generator, gene_lo: int, V_total: int):
         acc = np.zeros(ns)
         if lo_l < hi_l:
             gsums = []
-            for g0 in range(lo_l, hi_l, GROUP_CHUNKS * CHUNK_GENES):
-                csums = [terms[c0 - gene_lo: min(c0 + CHUNK_GENES, hi_l) - gene_lo].sum(axis=0)
-                         for c0 in range(g0, min(g0 + GROUP_CHUNKS * CHUNK_GENES, hi_l), CHUNK_GENES)]
+            for g0 in range(lo_l, hi_l, GROUP_GENES):
+                csums = [terms[c0 - gene_lo: min(c0 + cg, hi_l) - gene_lo].sum(axis=0)
+                         for c0 in range(g0, min(g0 + GROUP_GENES, hi_l), cg)]
                 gsums.append(warp_rows_sum(csums))
             acc = warp_rows_sum(gsums)
         octs.append(acc)
@@ -172,12 +181,13 @@ def streamed_stats(x, D, gen: Generator):
     V = x.shape[0]
     p = make_plan(V)
     ns = n_stats(D.shape[1])
-    step = GROUP_CHUNKS * CHUNK_GENES
+    step = GROUP_GENES
+    cg = plan_chunk_genes(V, D.shape[1])
     gsums = []
     for g0 in range(0, V, step):
         hi = min(g0 + step, V)
         t = gene_terms(x[g0:hi], D[g0:hi], gen)
-        gsums.append(warp_rows_sum([t[c0:c0 + CHUNK_GENES].sum(axis=0) for c0 in range(0, hi - g0, CHUNK_GENES)]))
+        gsums.append(warp_rows_sum([t[c0:c0 + cg].sum(axis=0) for c0 in range(0, hi - g0, cg)]))
     octs = []
     for o in range(N_OCTANTS):
         a, b = o * p.groups_per_octant, min((o + 1) * p.groups_per_octant, p.n_groups)

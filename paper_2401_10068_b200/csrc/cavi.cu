@@ -110,6 +110,7 @@ struct cv_dataset {
   double* r_raw = nullptr;
   double* mu_raw = nullptr;
   int64_t n_chunks = 0, n_groups = 0, group_lo = 0, n_groups_total = 0, groups_per_octant = 1;
+  int chunk_genes = kChunk, group_chunks = (int)(kGroupGenes / kChunk);
   int oct_lo = 0, oct_hi = kOctants;
   uint64_t* partials = nullptr;      // [n_chunks][ns][2] LL words
   uint64_t* gpartials = nullptr;     // [n_groups][ns][2] LL words
@@ -204,13 +205,17 @@ void count_live_octants(cv_dataset* ds) {
 
 int plan_and_alloc(cv_dataset* ds) {
   const int ns = n_stats(ds->d);
-  ds->n_chunks = (ds->V + kChunk - 1) / kChunk;
-  ds->Vp = ds->n_chunks * kChunk;
-  ds->n_groups = (ds->n_chunks + kGroupChunks - 1) / kGroupChunks;
-  const int64_t tot_chunks = std::max<int64_t>(1, (ds->V_total + kChunk - 1) / kChunk);
-  ds->n_groups_total = (tot_chunks + kGroupChunks - 1) / kGroupChunks;
+  // the chunk size depends only on (V_total, d): every shard of a dataset plans alike
+  ds->chunk_genes = plan_chunk_genes(ds->V_total, ds->d);
+  ds->group_chunks = (int)(kGroupGenes / ds->chunk_genes);
+  const int64_t cg = ds->chunk_genes, gc = ds->group_chunks;
+  ds->n_chunks = (ds->V + cg - 1) / cg;
+  ds->Vp = ds->n_chunks * cg;
+  ds->n_groups = (ds->n_chunks + gc - 1) / gc;
+  const int64_t tot_chunks = std::max<int64_t>(1, (ds->V_total + cg - 1) / cg);
+  ds->n_groups_total = (tot_chunks + gc - 1) / gc;
   ds->groups_per_octant = (ds->n_groups_total + kOctants - 1) / kOctants;
-  const int64_t group_genes = (int64_t)kGroupChunks * kChunk;
+  const int64_t group_genes = kGroupGenes;
   if (ds->V > 0 && ds->gene_lo % group_genes != 0)
     return fail(CV_ERR_ARG, "shard gene_lo %lld not group-aligned", (long long)ds->gene_lo);
   ds->group_lo = ds->gene_lo / group_genes;
@@ -284,6 +289,8 @@ PassArgs pass_args(cv_dataset* ds, double* rank_out) {
   a.D = ds->D;
   a.Vp = ds->Vp;
   a.n_chunks = ds->n_chunks;
+  a.chunk_genes = ds->chunk_genes;
+  a.group_chunks = ds->group_chunks;
   a.n_groups = ds->n_groups;
   a.group_lo = ds->group_lo;
   a.n_groups_total = ds->n_groups_total;
@@ -697,7 +704,7 @@ int32_t cv_dataset_set_shard(cv_dataset* ds, int32_t rank, int32_t world) {
     return fail(CV_ERR_ARG, "bad rank %d of world %d", rank, world);
   // the shard must be exactly this rank's octant span of the dataset plan
   const int per = kOctants / world;
-  const int64_t oct_genes = ds->groups_per_octant * (int64_t)kGroupChunks * kChunk;
+  const int64_t oct_genes = ds->groups_per_octant * kGroupGenes;
   const int64_t want_lo = std::min<int64_t>((int64_t)rank * per * oct_genes, ds->V_total);
   const int64_t want_hi = std::min<int64_t>((int64_t)(rank + 1) * per * oct_genes, ds->V_total);
   if (ds->gene_lo != want_lo && ds->V > 0) return fail(CV_ERR_ARG, "shard does not start at rank %d's octant span", rank);

@@ -25,8 +25,27 @@ namespace cavi {
 constexpr int kMaxD = CV_MAX_DIM;
 constexpr int kMaxD2 = CV_MAX_D2;
 constexpr int kMaxStats = kMaxD + kMaxD * (kMaxD + 1) / 2 + 3;  // 138
-constexpr int kChunk = 4096;         // genes per chunk (one reduction unit)
-constexpr int kGroupChunks = 64;     // chunks per group
+// Reduction plan: chunk (one partial row) -> group (kGroupGenes genes) -> octant -> total.
+// The chunk size is per dataset (plan_chunk_genes): 8192 genes halves the per-chunk finish
+// work, which pays wherever there are enough chunks to balance (V >= 2^23) and the sweep is
+// not purely bandwidth-trivial per gene (d >= 3): same-box A/B, V=1e8 (profiles/r02_c8k_ab.log):
+// N=8 822 -> 890 sweeps/s, N=13 375 -> 388, N=4 sustained 448 -> 443 us; N=2, 3 lose ~1.5% and
+// V <= 1e6 loses 15% (fewer chunks than CTAs), so those keep 4096.  Groups stay kGroupGenes
+// genes either way: shard and octant boundaries do not depend on the chunk size.
+constexpr int kChunk = 4096;                              // smallest chunk (genes)
+constexpr int64_t kGroupGenes = 262144;                   // genes per group (64 x 4096 = 32 x 8192)
+#ifndef CAVI_CHUNK_LARGE
+#define CAVI_CHUNK_LARGE 8192
+#endif
+#ifndef CAVI_CHUNK_LARGE_MIN_V
+#define CAVI_CHUNK_LARGE_MIN_V (1ll << 23)
+#endif
+#ifndef CAVI_CHUNK_LARGE_MIN_D
+#define CAVI_CHUNK_LARGE_MIN_D 3
+#endif
+inline int plan_chunk_genes(int64_t V_total, int d) {
+  return (d >= CAVI_CHUNK_LARGE_MIN_D && V_total >= CAVI_CHUNK_LARGE_MIN_V) ? CAVI_CHUNK_LARGE : kChunk;
+}
 constexpr int kOctants = 8;          // top of the reduction tree (GPU-count invariant)
 
 constexpr double kLn2 = 0.69314718055994530942;

@@ -42,6 +42,8 @@ struct PassArgs {
   const void* D;
   int64_t Vp;
   int64_t n_chunks;        // local chunks
+  int chunk_genes;         // genes per chunk (plan_chunk_genes: 4096 or 8192)
+  int group_chunks;        // chunks per group (kGroupGenes / chunk_genes)
   int64_t n_groups;        // local groups
   int64_t group_lo;        // global index of local group 0
   int64_t n_groups_total;  // groups of the whole dataset
@@ -357,9 +359,9 @@ __device__ __forceinline__ void finish_chunk_acqrel(const PassArgs& a, int64_t c
   constexpr int K = (NS + 31) / 32;
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) partials[chunk * NS + st] = chunk_sum[st];
-  const int64_t grp = chunk / kGroupChunks;
-  const int64_t c0 = grp * kGroupChunks;
-  const int64_t nc = lmin(c0 + kGroupChunks, a.n_chunks) - c0;
+  const int64_t grp = chunk / a.group_chunks;
+  const int64_t c0 = grp * a.group_chunks;
+  const int64_t nc = lmin(c0 + a.group_chunks, a.n_chunks) - c0;
   if (!warp_arrive_last(a.gcount + grp, (unsigned int)nc, lane)) return;
   // group complete
   if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
@@ -532,9 +534,9 @@ __device__ __forceinline__ void finish_chunk_ll(const PassArgs& a, int64_t chunk
   constexpr int K = (NS + 31) / 32;
   const unsigned long long t_entry = a.cta_trace ? globaltimer_ns() : 0ull;
   for (int st = lane; st < NS; st += 32) ll_put(a.partials + (chunk * NS + st) * 2, chunk_sum[st], tag);
-  const int64_t grp = chunk / kGroupChunks;
-  const int64_t c0 = grp * kGroupChunks;
-  const int64_t nc = lmin(c0 + kGroupChunks, a.n_chunks) - c0;
+  const int64_t grp = chunk / a.group_chunks;
+  const int64_t c0 = grp * a.group_chunks;
+  const int64_t nc = lmin(c0 + a.group_chunks, a.n_chunks) - c0;
   if (!warp_arrive_last_relaxed(a.gcount + grp, (unsigned int)nc, lane)) return;
   // group complete
   if (lane == 0) a.gcount[grp] = 0u;  // ready for the next sweep
@@ -1093,7 +1095,7 @@ struct Geometry {
   static constexpr int kTile = D <= 1 ? CAVI_TILE_TINY_D
                                : D <= 3 ? CAVI_TILE_SMALL_D
                                : kMma ? ((kSmallBlocks && D > 8) ? 128 : 256) : CAVI_TILE_MID;
-  static constexpr int kTilesPerChunk = kChunk / kTile;
+  static constexpr int kTilesPerChunk = kChunk / kTile;  // in the smallest chunk (a.chunk_genes / kTile at run time)
   static constexpr int kGenesPerThread = kTile / kCons;  // consumer genes per stage
   static constexpr uint32_t kColBytes = kTile * sizeof(T);
   // smem column stride (elements): +4 doubles for the DMMA fragment loads -> conflict-free banks
@@ -1175,6 +1177,7 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
   // under PDL this CTA is resident while the previous sweep's cascade and tail still run, and
   // HBM keeps streaming through them.
   constexpr int kPre = G::kStages < G::kTilesPerChunk ? G::kStages : G::kTilesPerChunk;
+  const int tiles_per_chunk = a.chunk_genes / G::kTile;  // >= G::kTilesPerChunk
   const bool producer = warp == kProducerWarp && lane == 0;
   const T* xs = static_cast<const T*>(a.x);
   const T* Ds = static_cast<const T*>(a.D);
@@ -1182,7 +1185,7 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
   auto issue = [&](int stage, int64_t chunk, int t) {
     stage_chunk[stage] = chunk;
     ptx::mbar_arrive_expect_tx(&full[stage], G::kTxBytes);
-    const int64_t g0 = chunk * kChunk + (int64_t)t * G::kTile;
+    const int64_t g0 = chunk * a.chunk_genes + (int64_t)t * G::kTile;
     T* dst = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
     ptx::bulk_g2s(dst, xs + g0, G::kColBytes, &full[stage], pol);
 #pragma unroll
@@ -1201,9 +1204,10 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
       const int64_t pc = n_static + (int64_t)p * gridDim.x + blockIdx.x;
       if (pc >= a.n_chunks) break;
       const uint64_t pn = ptx::policy_evict_normal();
-      ptx::bulk_prefetch_l2(xs + pc * kChunk, (uint32_t)(kChunk * sizeof(T)), pn);
+      ptx::bulk_prefetch_l2(xs + pc * a.chunk_genes, (uint32_t)(a.chunk_genes * sizeof(T)), pn);
 #pragma unroll
-      for (int j = 0; j < D; ++j) ptx::bulk_prefetch_l2(Ds + (int64_t)j * a.Vp + pc * kChunk, (uint32_t)(kChunk * sizeof(T)), pn);
+      for (int j = 0; j < D; ++j)
+        ptx::bulk_prefetch_l2(Ds + (int64_t)j * a.Vp + pc * a.chunk_genes, (uint32_t)(a.chunk_genes * sizeof(T)), pn);
     }
   }
   // everything above reads only the immutable stream or is CTA-local
@@ -1232,17 +1236,20 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
       };
       if (has_static) {
         for (int t = 0; t < kPre; ++t) advance();  // issued before the wait
-        for (int t = kPre; t < G::kTilesPerChunk; ++t) {
+        for (int t = kPre; t < tiles_per_chunk; ++t) {
           ptx::mbar_wait(&empty[stage], parity);
           issue(stage, (int64_t)blockIdx.x, t);
           advance();
         }
       }
+      // (a ticket is taken only when the previous chunk is fully issued: fetching it one chunk
+      // ahead deepens every CTA's queue by a chunk and costs ~4.5 us of end-of-pass imbalance
+      // per sweep at d = 3 -- profiles/r02_tpf_ab.log)
       for (;;) {
         const int64_t idx = (int64_t)(atomicAdd(a.ticket, 1ull) % period);
         const int64_t chunk = n_static + idx;
         const bool end = chunk >= a.n_chunks;
-        for (int t = 0; t < (end ? 1 : G::kTilesPerChunk); ++t) {
+        for (int t = 0; t < (end ? 1 : tiles_per_chunk); ++t) {
           ptx::mbar_wait(&empty[stage], parity);
           if (end) {
             stage_chunk[stage] = -1;
@@ -1289,7 +1296,7 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
     if constexpr (G::kMma) {
       mc.reset();
 #pragma unroll 1
-      for (int t = 0; t < G::kTilesPerChunk; ++t) {
+      for (int t = 0; t < tiles_per_chunk; ++t) {
         if (t) ptx::mbar_wait(&full[stage], parity);
         const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
         mc.template tile<T, G::kColStride>(tile, warp * (G::kTile / kWarps), G::kTile / kWarps / 8, lane);
@@ -1308,7 +1315,7 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
       LogAcc lg;
       lg.init();
 #pragma unroll 1
-      for (int t = 0; t < G::kTilesPerChunk; ++t) {
+      for (int t = 0; t < tiles_per_chunk; ++t) {
         if (t) ptx::mbar_wait(&full[stage], parity);
         const T* tile = stage_base + (size_t)stage * (G::kStageBytes / sizeof(T));
         double prod = 1.0;

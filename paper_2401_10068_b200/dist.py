@@ -6,7 +6,8 @@ The reference has no distributed mode (its "parallel" is a thread pool over
 301-328); this module scales the same deterministic contract across GPUs:
 
 * `plan` / `shard_ranges` -- the reduction plan every device shares:
-  4096-gene chunks, 64-chunk groups, 8 octants of whole groups.  Rank r of
+  262144-gene groups (of 4096- or 8192-gene chunks, engine.cuh plan_chunk_genes),
+  8 octants of whole groups.  Rank r of
   a world of 1/2/4/8 owns octants [8r/W, 8(r+1)/W), i.e. a contiguous gene
   range; its partial is the octant subtree the single-GPU tree would build,
   so totals -- and therefore every state, ELBO and stop decision -- are
