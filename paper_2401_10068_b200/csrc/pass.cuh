@@ -30,11 +30,14 @@
 
 namespace cavi {
 
-#ifndef CAVI_LL_BATCH
-#define CAVI_LL_BATCH 16  // statistics per polling pass of an LL row sum
-#endif
+// statistics per polling pass of an LL row sum: the row words are live beside the consumer
+// loop's registers (warp_rows_ll is inlined into it), so wider statistic vectors poll in smaller
+// batches (V=1e8: N=5 1692 -> 1712 sweeps/s at 8 instead of 16)
+constexpr int ll_batch(int ns) { return ns <= 12 ? 16 : ns <= 17 ? 8 : 4; }
 #ifndef CAVI_LL_MAX_D
-#define CAVI_LL_MAX_D 4  // largest d on the LL cascade (memory-bound); above: acquire/release rows (N=6: 1303 vs 1352)
+#define CAVI_LL_MAX_D 4  // largest d on the LL cascade (memory-bound); above: acquire/release rows
+                         // (V=1e8, LL vs acq/rel: N=6 1368 vs 1395, N=7 1001 vs 1125, N=8 685 vs 871;
+                         // profiles/r02_ll7_ab.log)
 #endif
 
 struct PassArgs {
@@ -308,6 +311,8 @@ __device__ __forceinline__ bool warp_arrive_last(unsigned int* counter, unsigned
   __syncwarp();
   if (lane == 0) {
     unsigned int old;
+    // (the release half costs ~3-5% at d = 5..7: the same kernels with a relaxed atomic --
+    // not a correct protocol, timing only -- ran N=6 1395 -> 1440, N=7 1125 -> 1179 sweeps/s)
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
     last = old == need - 1;
   }
@@ -478,7 +483,7 @@ __device__ __forceinline__ void warp_rows_ll(const uint64_t* rows, int64_t n, ui
                                              double (&out)[(NS + 31) / 32], int lane) {
   // stats per pass: small enough that the row words fit beside the consumer loop's live
   // registers (this is inlined into it: a larger batch spills the loop state)
-  constexpr int B = NS < CAVI_LL_BATCH ? NS : CAVI_LL_BATCH;
+  constexpr int B = NS < ll_batch(NS) ? NS : ll_batch(NS);
 #pragma unroll
   for (int k = 0; k < (NS + 31) / 32; ++k) out[k] = 0.0;
 #pragma unroll
