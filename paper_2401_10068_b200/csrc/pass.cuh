@@ -1073,6 +1073,10 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #define CAVI_MIN_BLOCKS 2  // CTAs per SM
 #endif
 
+#ifndef CAVI_REDUCER_WARP
+#define CAVI_REDUCER_WARP 1
+#endif
+
 #ifndef CAVI_MMA_MIN_D
 #define CAVI_MMA_MIN_D 8  // smallest d served by the DMMA consumer (V=1e8 sweeps/s, register vs DMMA:
                           // d=6 1038 vs 695, d=7 771 vs 677, d=8 565 vs 646)
@@ -1092,8 +1096,8 @@ struct Geometry {
   static constexpr bool kMma = D >= CAVI_MMA_MIN_D;
   static constexpr int kCons = kMma ? CAVI_MMA_CONS : CAVI_CONS;
   static constexpr int kCWarps = kCons / 32;
-  static constexpr int kCtaThreads = kCons + 32;  // + 1 TMA producer warp
   static constexpr int kProducerWarp = kCWarps;
+  static constexpr int kReducerWarp = kCWarps + 1;
   // small d: per-thread register kernel; larger d: fp64 tensor-core (DMMA) consumer
   static constexpr bool kSmallBlocks = kMma && D <= CAVI_MMA_SMALL_MAXD;
   // genes per stage; 3 CTAs/SM of the 16-column DMMA stages need half-size tiles
@@ -1119,6 +1123,14 @@ struct Geometry {
                                    : D == 2     ? CAVI_D2_BLOCKS
                                    : D == 4     ? CAVI_D4_BLOCKS
                                                 : CAVI_MIN_BLOCKS;
+  // A reducer warp takes each chunk's slot sum and the reduction cascade off the consumers
+  // (the finishing consumer's cascade work -- at d >= 5 the acquire/release arrival's fence --
+  // stalled it and, through the shared stage ring, the whole CTA).  Where the 32 extra threads
+  // fit the register budget: the register path at 2 CTAs/SM (V=1e8: N=4 2240 -> 2253 sweeps/s,
+  // 1.25e7 genes 70.0 -> 67.9 us; N=6 1395 -> 1444, N=7 1124 -> 1216, N=8 871 -> 920).  At 3-4
+  // CTAs/SM (d = 1, 2, 4, DMMA d <= 9) it forces spills: -2 to -16%; DMMA d >= 10: +-1.5%.
+  static constexpr bool kReducer = CAVI_REDUCER_WARP && !kMma && D >= 3 && kMinBlocks <= 2;
+  static constexpr int kCtaThreads = kCons + 32 + (kReducer ? 32 : 0);  // + 1 TMA producer warp (+ reducer)
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
   static constexpr int kDrift = (kSlots - 1) * kTilesPerChunk;
@@ -1144,8 +1156,12 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
   constexpr int kThreads = G::kCons;
   constexpr int kProducerWarp = G::kProducerWarp;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ double s_red[kWarps][NS];  // per-warp chunk sum / final totals
+  __shared__ double s_red[kWarps + 1][NS];  // per-warp chunk sum / final totals (+ the reducer's)
   __shared__ unsigned int s_cnt[kSlots];
+  // reducer hand-off (G::kReducer): slot q holds chunk red_chunk[q] once red_full[q] completes
+  // (one arrival per consumer warp); the reducer releases it through red_empty[q]
+  __shared__ uint64_t red_full[kSlots], red_empty[kSlots];
+  __shared__ int64_t red_chunk[kSlots];
   T* stage_base = reinterpret_cast<T*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::kOffBar);
   uint64_t* empty = full + G::kStages;
@@ -1162,6 +1178,11 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
       ptx::mbar_init(&empty[q], kWarps);
     }
     for (int q = 0; q < kSlots; ++q) s_cnt[q] = 0u;
+    if constexpr (G::kReducer)
+      for (int q = 0; q < kSlots; ++q) {
+        ptx::mbar_init(&red_full[q], kWarps);
+        ptx::mbar_init(&red_empty[q], 1);
+      }
     ptx::fence_mbar_init();
   }
   if constexpr (G::kCols > D) {  // zero the padding columns once: TMA never writes them
@@ -1271,6 +1292,34 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
     return;
   }
 
+  const uint32_t tag = *(volatile const unsigned int*)a.pass_seq;  // LL tag of this pass
+  if constexpr (G::kReducer) {
+    if (warp == G::kReducerWarp) {
+      // ---------------- reducer: chunk n's slot -> warp-order sum -> the cascade (finish_chunk)
+      if (fit_done) return;
+      double* mine = s_red[kWarps];
+#pragma unroll 1
+      for (int n = 0;; ++n) {
+        const int q = n % kSlots;
+        ptx::mbar_wait(&red_full[q], (uint32_t)((n / kSlots) & 1));
+        const int64_t chunk = red_chunk[q];
+        if (chunk < 0) break;
+        const double* slot = slots + (size_t)q * kWarps * NS;
+        for (int st = lane; st < NS; st += 32) {
+          double v = slot[st];
+#pragma unroll
+          for (int w = 1; w < kWarps; ++w) v += slot[w * NS + st];
+          mine[st] = v;
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&red_empty[q]);  // the slot may be refilled
+        finish_chunk<D>(a, chunk, mine, tag, lane);
+        __syncwarp();
+      }
+      return;
+    }
+  }
+
   // ---------------- consumers: independent warps, no CTA barrier in the steady state
   constexpr bool kSmemCoef = !G::kMma && D >= CAVI_SMEM_COEF_MIN_D;
   __shared__ GeneCoef<kSmemCoef ? D : 1> s_coef[kSmemCoef ? kWarps : 1];
@@ -1287,7 +1336,6 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
   GeneCoefF<kF32Math ? D : 1> kf;
   if constexpr (kF32Math) load_coef_f<D>(kf, ctl->pass);
   const double k_erho = ctl->pass.e_rho;
-  const uint32_t tag = *(volatile const unsigned int*)a.pass_seq;  // LL tag of this pass
   if (fit_done) return;
   const int tid = threadIdx.x;  // 0 .. kThreads-1
   int stage = 0;
@@ -1298,6 +1346,8 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
     const int64_t chunk = stage_chunk[stage];
     if (chunk < 0) break;
     double* slot = slots + (size_t)(n_done % kSlots) * kWarps * NS;
+    if constexpr (G::kReducer)  // the reducer has read this slot's previous chunk (fresh: free)
+      ptx::mbar_wait(&red_empty[n_done % kSlots], (uint32_t)(((n_done / kSlots) & 1) ^ 1));
     if constexpr (G::kMma) {
       mc.reset();
 #pragma unroll 1
@@ -1409,6 +1459,15 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
         if (lane == (i & 31)) slot[warp * NS + i] = v;
       }
     }
+    if constexpr (G::kReducer) {  // hand the chunk to the reducer warp and carry on streaming
+      __syncwarp();
+      if (lane == 0) {
+        if (warp == 0) red_chunk[n_done % kSlots] = chunk;
+        ptx::mbar_arrive(&red_full[n_done % kSlots]);
+      }
+      ++n_done;
+      continue;
+    }
     // the last warp to finish the chunk sums the 8 warp slots (warp order) and carries on up
     unsigned int last = 0;
     __syncwarp();
@@ -1432,6 +1491,15 @@ __global__ void __launch_bounds__(Geometry<D, T, M>::kCtaThreads, Geometry<D, T,
       finish_chunk<D>(a, chunk, mine, tag, lane);
     }
     ++n_done;
+  }
+  if constexpr (G::kReducer) {  // end of the stream: a chunk id of -1 ends the reducer
+    const int q = n_done % kSlots;
+    ptx::mbar_wait(&red_empty[q], (uint32_t)(((n_done / kSlots) & 1) ^ 1));
+    __syncwarp();
+    if (lane == 0) {
+      if (warp == 0) red_chunk[q] = -1;
+      ptx::mbar_arrive(&red_full[q]);
+    }
   }
   if (a.cta_trace && tid == 0) {
     a.cta_trace[blockIdx.x * 8 + 2] = globaltimer_ns();
