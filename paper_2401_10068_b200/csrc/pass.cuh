@@ -710,7 +710,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 #define CAVI_D2_BLOCKS 3  // CTAs per SM at d = 2 (118 registers; N=3: 2536 -> 2829 sweeps/s)
 #endif
 #ifndef CAVI_D4_BLOCKS
-#define CAVI_D4_BLOCKS 3  // CTAs per SM at d = 4 (128 registers; N=5: 1507 -> 1564 sweeps/s; d = 5 spills at 3)
+#define CAVI_D4_BLOCKS 2  // CTAs per SM at d = 4: 2 + the reducer warp (N=5 1713 -> 1751 sweeps/s) over 3 without
 #endif
 #ifndef CAVI_TILE_MID
 #define CAVI_TILE_MID 512  // genes per stage of the register path at d = 4, 5
@@ -1076,6 +1076,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_REDUCER_WARP
 #define CAVI_REDUCER_WARP 1
 #endif
+#ifndef CAVI_REDUCER_MIN_D
+#define CAVI_REDUCER_MIN_D 3
+#endif
 
 #ifndef CAVI_MMA_MIN_D
 #define CAVI_MMA_MIN_D 8  // smallest d served by the DMMA consumer (V=1e8 sweeps/s, register vs DMMA:
@@ -1129,7 +1132,7 @@ struct Geometry {
   // fit the register budget: the register path at 2 CTAs/SM (V=1e8: N=4 2240 -> 2253 sweeps/s,
   // 1.25e7 genes 70.0 -> 67.9 us; N=6 1395 -> 1444, N=7 1124 -> 1216, N=8 871 -> 920).  At 3-4
   // CTAs/SM (d = 1, 2, 4, DMMA d <= 9) it forces spills: -2 to -16%; DMMA d >= 10: +-1.5%.
-  static constexpr bool kReducer = CAVI_REDUCER_WARP && !kMma && D >= 3 && kMinBlocks <= 2;
+  static constexpr bool kReducer = CAVI_REDUCER_WARP && !kMma && D >= CAVI_REDUCER_MIN_D && kMinBlocks <= 2;
   static constexpr int kCtaThreads = kCons + 32 + (kReducer ? 32 : 0);  // + 1 TMA producer warp (+ reducer)
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
