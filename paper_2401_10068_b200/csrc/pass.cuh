@@ -1079,6 +1079,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_REDUCER_MIN_D
 #define CAVI_REDUCER_MIN_D 3
 #endif
+#ifndef CAVI_REDUCER_MMA_MAXD
+#define CAVI_REDUCER_MMA_MAXD 14  // DMMA path at 2 CTAs/SM (d >= 10): N=11 461 -> 481, N=15 299 -> 307; d = 15 -0.3%
+#endif
 
 #ifndef CAVI_MMA_MIN_D
 #define CAVI_MMA_MIN_D 8  // smallest d served by the DMMA consumer (V=1e8 sweeps/s, register vs DMMA:
@@ -1129,10 +1132,11 @@ struct Geometry {
   // A reducer warp takes each chunk's slot sum and the reduction cascade off the consumers
   // (the finishing consumer's cascade work -- at d >= 5 the acquire/release arrival's fence --
   // stalled it and, through the shared stage ring, the whole CTA).  Where the 32 extra threads
-  // fit the register budget: the register path at 2 CTAs/SM (V=1e8: N=4 2240 -> 2253 sweeps/s,
-  // 1.25e7 genes 70.0 -> 67.9 us; N=6 1395 -> 1444, N=7 1124 -> 1216, N=8 871 -> 920).  At 3-4
-  // CTAs/SM (d = 1, 2, 4, DMMA d <= 9) it forces spills: -2 to -16%; DMMA d >= 10: +-1.5%.
-  static constexpr bool kReducer = CAVI_REDUCER_WARP && !kMma && D >= CAVI_REDUCER_MIN_D && kMinBlocks <= 2;
+  // fit the register budget: 2 CTAs/SM (V=1e8: N=4 2240 -> 2253 sweeps/s, 1.25e7 genes 70.0 ->
+  // 67.9 us; N=6 1395 -> 1444, N=7 1124 -> 1216, N=8 871 -> 920; DMMA d = 10..14 +0.5..4%).  At
+  // 3-4 CTAs/SM (d = 1, 2, DMMA d <= 9) it forces spills: -2 to -16% (profiles/r02_reducer_*).
+  static constexpr bool kReducer =
+      CAVI_REDUCER_WARP && (!kMma || D <= CAVI_REDUCER_MMA_MAXD) && D >= CAVI_REDUCER_MIN_D && kMinBlocks <= 2;
   static constexpr int kCtaThreads = kCons + 32 + (kReducer ? 32 : 0);  // + 1 TMA producer warp (+ reducer)
   static constexpr int kBudget = (kMinBlocks > 2 ? 210000 / kMinBlocks : CAVI_SMEM_BUDGET) - kSlotBytes;
   static constexpr int kFit = kBudget / (int)kStageBytes;
