@@ -143,10 +143,13 @@ def test_fp32_storage_within_1e4(eng, N):
     close(s32.b_rho, s64.b_rho, rtol=1e-4)
 
 
-def test_run_to_run_bit_identical(eng):
+@pytest.mark.parametrize("V,N", [(1_000_003, 4), (9_000_001, 4), (9_000_001, 8), (9_000_001, 13)])
+def test_run_to_run_bit_identical(eng, V, N):
+    """Dynamic chunk tickets, the reducer warp and the LL / acquire-release cascades never change a
+    bit: every sum is the plan's fixed tree (4096- and 8192-gene chunks)."""
     vb, model = eng
-    dd = model.regime(1_000_003, 5, 4)
-    hp = model.default_hyperparams(4)
+    dd = model.regime(V, 5, N)
+    hp = model.default_hyperparams(N)
     a, ta = vb.vb_fit(dd, hp, max_iter=10)
     b, tb = vb.vb_fit(dd, hp, max_iter=10)
     assert np.array_equal(ta.elbo, tb.elbo) and np.array_equal(a.lam0l_inv, b.lam0l_inv)

@@ -20,7 +20,10 @@ def tree(parts):
     return parts[0]
 
 
-@pytest.mark.parametrize("V,N", [(3_000_001, 4), (777_777, 3), (20_000, 6)])
+# 9_000_001 genes (>= 2^23): 8192-gene chunks, the reducer warp on the LL (d=3), acquire/release
+# (d=7) and DMMA (d=12) paths
+@pytest.mark.parametrize("V,N", [(3_000_001, 4), (777_777, 3), (20_000, 6), (9_000_001, 4), (9_000_001, 8),
+                                 (9_000_001, 13)])
 def test_shard_partials_combine_bit_exact(V, N):
     from oracle import fused
     from paper_2401_10068_b200 import _lib, dist, model, vb
