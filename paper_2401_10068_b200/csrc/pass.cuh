@@ -1060,6 +1060,9 @@ constexpr int kSlots = 4;  // chunk-reduction slots (warps drift < kStages tiles
 #ifndef CAVI_F32_BLOCKS
 #define CAVI_F32_BLOCKS 3  // CTAs per SM on the fp32 stream, fp64 math (V=1e8 N=4: 2 -> 3: 2178 -> 2475 sweeps/s)
 #endif
+#ifndef CAVI_F32_D3_BLOCKS
+#define CAVI_F32_D3_BLOCKS 2  // ... at d = 3: 2 + the reducer warp (2678 -> 2930 sweeps/s); d = 1, 2 lose at 2 (4710 -> 3840)
+#endif
 #ifndef CAVI_F32M_BLOCKS
 #define CAVI_F32M_BLOCKS 3  // ... and with fp32 math (2 -> 4: 2272 -> 3034 sweeps/s; + 16-byte loads, MUFU rcp: 3546 at 4, 3542 at 3)
 #endif
@@ -1124,7 +1127,7 @@ struct Geometry {
   // the DMMA kernels at d <= 8 (~110 registers) are latency-bound at 2 CTAs/SM: run 3
   static constexpr int kMinBlocks = kSmallBlocks ? CAVI_MMA_SMALL_BLOCKS
                                    : (sizeof(T) == 4 && sizeof(M) == 4 && D <= CAVI_F32_BLOCKS_MAXD) ? CAVI_F32M_BLOCKS
-                                   : (sizeof(T) == 4 && D <= CAVI_F32_BLOCKS_MAXD) ? CAVI_F32_BLOCKS
+                                   : (sizeof(T) == 4 && D <= CAVI_F32_BLOCKS_MAXD) ? (D >= 3 ? CAVI_F32_D3_BLOCKS : CAVI_F32_BLOCKS)
                                    : D <= 1     ? CAVI_TINY_BLOCKS
                                    : D == 2     ? CAVI_D2_BLOCKS
                                    : D == 4     ? CAVI_D4_BLOCKS
