@@ -215,11 +215,13 @@ def test_max_iter_validated(E):  # test_em.py:133-137
         E.em.em_fit(ds, init_params(E, E.model.default_hyperparams(3)), max_iter=0)
 
 
-def test_em_at_scale_matches_fused_oracle_step(E):
-    """One em_step on 1e6 device-generated genes vs the oracle's float64 step on the same data."""
+@pytest.mark.parametrize("V", [1_000_000, 9_000_001])
+def test_em_at_scale_matches_fused_oracle_step(E, V):
+    """One em_step on device-generated genes vs the oracle's float64 step on the same data
+    (9_000_001 genes: the 8192-gene chunk plan and the reducer warp)."""
     from paper_2401_10068_b200 import model
 
-    V, N = 1_000_000, 4
+    N = 4
     r, mu, D, K, lam = philox.make_regime(V, 77, N)
     ds = host_ds(E, r, mu, D)
     p = model.ModelParams(K=K, Lam=lam, rho=100.0)
