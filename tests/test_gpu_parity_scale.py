@@ -148,6 +148,24 @@ def test_config3_v1e7_matches_reference_oracle(eng):
     close(st.e_bbt[idx], so.e_bbt[idx], RTOL, "e_bbt")
 
 
+@pytest.mark.parametrize("N", [6, 8])
+def test_large_v_reducer_paths_match_fused_oracle(eng, N):
+    """9e6 genes (>= 2^23: 8192-gene chunks) through the reducer warp on the acquire/release
+    cascade (d = 5, 7): 3 sweeps against the fused oracle plan (the DMMA path at this size: the
+    shard and run-to-run bit-identity tests)."""
+    vb, model = eng
+    V, iters = 9_000_001, 3
+    dd = model.regime(V, 7 + N, N)
+    st, tr = vb.vb_fit(dd, model.default_hyperparams(N), max_iter=iters)
+    r, mu, D = dd.download()
+    dd.close()
+    so, to, n = _fused_fit_streamed(r, mu, D, N, iters)
+    assert len(tr) == n == iters
+    np.testing.assert_allclose(tr.elbo, to["elbo"], rtol=RTOL, atol=0)
+    for name in ("b_rho", "k0k", "lam0l_inv", "e_lam", "e_rho"):
+        close(getattr(st, name), getattr(so, name), RTOL, name)
+
+
 # ------------------------------------------------------------------ config 5
 @pytest.mark.parametrize("N,V,iters", [(10, 3000, 6), (11, 2500, 6), (13, 2000, 6), (14, 2000, 5), (15, 2000, 5)])
 def test_k_sweep_fits_match_reference_oracle(eng, N, V, iters):
