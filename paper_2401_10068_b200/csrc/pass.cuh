@@ -644,6 +644,8 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
   constexpr int NS = n_stats(D);
   __shared__ TailSm<D> sm;
   ptx::griddep_launch_dependents();  // the next pass may launch and stage its prologue
+  TailHyp<D> th;                     // constant through the fit: loaded while the pass streams
+  th.load(h, threadIdx.x);
   ptx::griddep_wait();               // the pass (or exchange) that produced `parts` is complete
   if (threadIdx.x == 0) TAIL_PROF(*c, 0);
   const unsigned long long t_entry = globaltimer_ns();  // diagnostics (stored at exit: no load on the critical path)
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(32, 1) tail_kernel(const Hyp* __restrict__ h, 
     if (threadIdx.x == 0) *lsa.seq = s;
     parts = nullptr;  // sm.tot is complete
   }
-  tail_warp<D>(h, c, parts, world, sm, threadIdx.x);
+  tail_warp<D>(th, c, parts, world, sm, threadIdx.x);
   if (threadIdx.x == 0) {
     unsigned long long* tl = c->tl_trace;
     if (tl) {

@@ -203,13 +203,42 @@ __device__ __forceinline__ void em_tail_warp(Ctl* c, TailSm<D>& sm, int lane, do
   }
 }
 
+// The hyperparameter words the tail reads.  They are constant through a fit (set up before its
+// first pass), so tail_kernel loads them BEFORE griddepcontrol.wait -- under programmatic
+// dependent launch while the pass still streams -- and the post-wait burst is only the control
+// block, the previous state and the pass's statistics.
+template <int D>
+struct TailHyp {
+  WarpLoad<D> K0;
+  WarpLoad<D * D> L0, L0i;
+  double V, nu, qv, q0;
+  double a0 = 0, b0 = 0, lnL0 = 0, a_fit = 0, ln_nu = 0, dg_afit = 0, lg_afit = 0, dg_a0 = 0, lg_a0 = 0, sum_dg_nu = 0,
+         ln_q0 = 0, ln_qv = 0, ln_b0 = 0, zprior = 0, mgl_nu = 0;
+  int n0 = 0, has_zprior = 0, proper_q = 1;
+  __device__ __forceinline__ void load(const Hyp* __restrict__ hp, int lane) {
+    K0.load(hp->K0, lane);
+    L0.load(hp->L0, lane);
+    L0i.load(hp->L0inv, lane);
+    V = hp->V;
+    nu = hp->nu;
+    qv = hp->qv;
+    q0 = hp->q0;
+    if (lane == 0) {  // lane 0's scalars: every hyperparameter constant the bound uses
+      a0 = hp->a0; b0 = hp->b0; lnL0 = hp->lnL0; a_fit = hp->a_fit; ln_nu = hp->ln_nu;
+      dg_afit = hp->dg_afit; lg_afit = hp->lg_afit; dg_a0 = hp->dg_a0; lg_a0 = hp->lg_a0; sum_dg_nu = hp->sum_dg_nu;
+      ln_q0 = hp->ln_q0; ln_qv = hp->ln_qv; ln_b0 = hp->ln_b0; zprior = hp->zprior; mgl_nu = hp->mgl_nu;
+      n0 = hp->n0; has_zprior = hp->has_zprior; proper_q = hp->proper_q;
+    }
+  }
+};
+
 // The sweep tail (MODE_SWEEP, MODE_INIT, MODE_ELBO, MODE_EM) run by one warp.  `parts` holds
 // the `world` rank partials to combine into sm.tot, unless the fused exchange already did
 // (parts == nullptr).  Every global word the tail needs -- including the done flag, which is
 // tested only afterwards -- is requested in ONE burst: the tail pays one L2 round trip for its
 // inputs, not one per dependent step.
 template <int D>
-__device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, const double* __restrict__ parts, int world,
+__device__ __forceinline__ void tail_warp(const TailHyp<D>& th, Ctl* c, const double* __restrict__ parts, int world,
                                        TailSm<D>& sm, int lane) {
   constexpr int NS = n_stats(D);
   constexpr int D2 = D * D;
@@ -224,33 +253,27 @@ __device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, co
       for (int r = 0; r < kOctants; ++r)
         if (r < world && lane + 32 * k < NS) v[k][r] = __ldcg(parts + r * NS + lane + 32 * k);
   }
-  WarpLoad<D> l_gc, l_ko, l_K0;
-  WarpLoad<D2> l_gA, l_gAi, l_lo, l_L0, l_L0i;
+  WarpLoad<D> l_gc, l_ko;
+  WarpLoad<D2> l_gA, l_gAi, l_lo;
   l_gc.load(c->pass.c, lane);
   l_gA.load(c->pass.A, lane);
   l_gAi.load(c->pass.Ainv, lane);
   l_ko.load(s.k0k, lane);
   l_lo.load(s.lam0l_inv, lane);
-  l_K0.load(hp->K0, lane);
-  l_L0.load(hp->L0, lane);
-  l_L0i.load(hp->L0inv, lane);
   const int done_in = *(volatile const int*)&c->done;
   const int mode = c->mode;
-  const double V = hp->V, nu = hp->nu, qv = hp->qv, q0 = hp->q0;
-  // lane 0's scalars: the control block, the trace pointers, the previous state, and every
-  // hyperparameter constant the bound uses
-  double a0 = 0, b0 = 0, lnL0 = 0, a_fit = 0, ln_nu = 0, pend_a = 0, pend_b = 0, prev_elbo = 0, rel_tol = 0,
-         param_tol = 0, g_lnA = 0, g_erho = 0, e_rho_old = 0, a_old = 0, b_old = 0, ld_old = 0;
-  double dg_afit = 0, lg_afit = 0, dg_a0 = 0, lg_a0 = 0, sum_dg_nu = 0, ln_q0 = 0, ln_qv = 0, ln_b0 = 0, zprior = 0,
-         mgl_nu = 0;
-  int compute_elbo = 0, have_prev = 0, iter = 0, max_iter = 0, tr_cap = 0, n_iter_old = 0, n0 = 0, has_zprior = 0,
-      proper_q = 1;
+  const double V = th.V, nu = th.nu, qv = th.qv, q0 = th.q0;
+  const double a0 = th.a0, b0 = th.b0, lnL0 = th.lnL0, a_fit = th.a_fit, ln_nu = th.ln_nu;
+  const double dg_afit = th.dg_afit, lg_afit = th.lg_afit, dg_a0 = th.dg_a0, lg_a0 = th.lg_a0,
+               sum_dg_nu = th.sum_dg_nu, ln_q0 = th.ln_q0, ln_qv = th.ln_qv, ln_b0 = th.ln_b0, zprior = th.zprior,
+               mgl_nu = th.mgl_nu;
+  const int n0 = th.n0, has_zprior = th.has_zprior, proper_q = th.proper_q;
+  // lane 0's scalars: the control block, the trace pointers and the previous state
+  double pend_a = 0, pend_b = 0, prev_elbo = 0, rel_tol = 0, param_tol = 0, g_lnA = 0, g_erho = 0, e_rho_old = 0,
+         a_old = 0, b_old = 0, ld_old = 0;
+  int compute_elbo = 0, have_prev = 0, iter = 0, max_iter = 0, tr_cap = 0, n_iter_old = 0;
   double *tr_elbo = nullptr, *tr_dk = nullptr, *tr_drho = nullptr, *tr_dlam = nullptr, *tr_k = nullptr;
   if (lane == 0) {
-    a0 = hp->a0; b0 = hp->b0; lnL0 = hp->lnL0; a_fit = hp->a_fit; ln_nu = hp->ln_nu;
-    dg_afit = hp->dg_afit; lg_afit = hp->lg_afit; dg_a0 = hp->dg_a0; lg_a0 = hp->lg_a0; sum_dg_nu = hp->sum_dg_nu;
-    ln_q0 = hp->ln_q0; ln_qv = hp->ln_qv; ln_b0 = hp->ln_b0; zprior = hp->zprior; mgl_nu = hp->mgl_nu;
-    n0 = hp->n0; has_zprior = hp->has_zprior; proper_q = hp->proper_q;
     pend_a = c->pend_a; pend_b = c->pend_b; prev_elbo = c->prev_elbo; rel_tol = c->rel_tol; param_tol = c->param_tol;
     compute_elbo = c->compute_elbo; have_prev = c->have_prev; iter = c->iter; max_iter = c->max_iter;
     tr_cap = c->tr_cap; n_iter_old = s.n_iter;
@@ -263,9 +286,9 @@ __device__ __forceinline__ void tail_warp(const Hyp* __restrict__ hp, Ctl* c, co
   l_gAi.store(sm.gAi, lane);
   l_ko.store(sm.k_old, lane);
   l_lo.store(sm.l_old, lane);
-  l_K0.store(sm.K0, lane);
-  l_L0.store(sm.L0, lane);
-  l_L0i.store(sm.L0i, lane);
+  th.K0.store(sm.K0, lane);
+  th.L0.store(sm.L0, lane);
+  th.L0i.store(sm.L0i, lane);
   if (parts) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
