@@ -37,6 +37,9 @@ METRIC = "CAVI iters/sec at N=1e8,K=4 (1/2/4/8 GPU, % HBM peak); time to ELBO co
 UNIT = "iters/s"
 SEED = 2026
 NOMINAL_HBM_GBS = 7700.0  # B200 HBM3e, HGX figure (/opt/skills/guides/B200_PROFILING.md)
+# pure-read ceiling measured on this GPU type: a bare 16-byte-load reduction over 3.2 GB
+# (tools/read_bw.cu, profiles/r02f_read_bw_ceiling.txt) -- the bound a read stream can reach
+READ_CEILING_GBS = 7251.0
 
 
 def parse():
@@ -325,6 +328,7 @@ def run_ours(args):
                      "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (read+write) benchmark; this pass is a pure "
                                   "read stream, which the HBM serves faster: frac can exceed 1",
                      "peak_nominal": NOMINAL_HBM_GBS, "frac_nominal": achieved / NOMINAL_HBM_GBS,
+                     "peak_read_measured": READ_CEILING_GBS, "frac_read": achieved / READ_CEILING_GBS,
                      "bytes_per_launch": bytes_sweep, "kernel_ms": kern_s * 1e3},
         "clocks": clk.summary(),
     }
